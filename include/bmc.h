@@ -1,0 +1,138 @@
+/*
+ * bmc.h -- C-ABI of the B200-native batch multi-convex trajectory optimiser
+ * (the batched alternating-minimisation iteration of arXiv 2109.13030,
+ * Rastgar et al., "GPU Accelerated Batch Multi-Convex Trajectory
+ * Optimization for a Rectangular Holonomic Mobile Robot").
+ *
+ * Citations "P:n" are lines of the paper's LaTeX source; equation
+ * numbers follow its source order.  Readings "Gk" of ambiguous passages are
+ * listed in DESIGN.md ("Readings of the paper").
+ *
+ * What a solve computes, per batch instance l ("l trajectory
+ * optimizations in parallel"; all instances share the boundary conditions
+ * and the obstacles; they differ in their initial samples):
+ *
+ *   xi1 = (c_x, c_c, c_y, c_s), xi2 = c_psi: Bernstein coefficients of x, the
+ *   copy c ~ cos psi, y, the copy s ~ sin psi, and psi (Eq. 8-9).
+ *   Initialisation (G15): xi2 := c_psi^0, xi3/xi4 := closed forms on
+ *   the initial trajectory (c_c = c_s = 0), lambda := lambda_in or 0.
+ *   Then `iters` AM iterations, each:
+ *     1. xi1 <- KKT solve of Eq. 13/17 (one-shot form Eq. 4)
+ *     2. theta = atan2(P c_s, P c_c); xi2 <- KKT solve of Eq. 19
+ *     3. alpha_ij, alpha_v, alpha_a closed forms, Eq. 21a-c
+ *     4. d_ij >= 1, d_v, d_a in [0,1] closed forms, Eq. 22a-c + clip
+ *     5. lambda <- lambda - rho F^T (F xi1 - g)             Eq. 23a (G3)
+ *        lambda_psi <- lambda_psi - rho_psi P^T (P xi2 - theta)  Eq. 23b (G4)
+ *   Outputs: coefficients, multipliers, residuals r1 = ||F xi1 - g||_2 and
+ *   r_psi = ||theta - P xi2||_2 (Eq. 12), cost
+ *   J = sum_t (xdd^2 + ydd^2 + psidd^2) (Eq. 1a) and the batch argmin
+ *   ("best cost trajectory"; rule G17).
+ *
+ * Threading / streams: every function is re-entrant across contexts.  Calls
+ * of bmc_solve on ONE context must be ordered on one stream (they share the
+ * context's argmin workspace).  bmc_last_error() is thread-local.
+ */
+#ifndef BMC_H
+#define BMC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (int32) ------------------------------------------------ */
+#define BMC_OK 0
+#define BMC_EINVAL 1      /* invalid argument; bmc_last_error() names it          */
+#define BMC_ESINGULAR 2   /* boundary rows rank-deficient or KKT singular */
+#define BMC_ECUDA 3       /* CUDA runtime error (message from cudaGetErrorString) */
+#define BMC_ENOMEM 4      /* host or device allocation failed                      */
+
+/* Opaque context, owned by the library: host fp64 constants, the per-n_obs
+ * device constant blobs (Q_bar depends on n through F^T F) and the
+ * argmin workspace. */
+typedef struct bmc_ctx bmc_ctx;
+
+/* Stream handle: a cudaStream_t / CUstream (NULL = legacy default stream). */
+typedef struct CUstream_st* bmc_stream_t;
+
+/* Problem constants shared by every solve on the context (bmc_setup). */
+typedef struct {
+  int32_t q;               /* time samples on [0, T], t_k = k T/(q-1); 3 <= q <= 128      */
+  double T;                /* horizon [s] > 0 ("around 30s")                        */
+  int32_t degree;          /* Bernstein degree, must be 10 (n_v = 11; G12)               */
+  int32_t m;               /* footprint circles, 1 <= m <= 8                      */
+  const double* r;         /* [m] circle offsets along the heading axis [m]; copied      */
+  double v_max, a_max;     /* Eq. 1c bounds, > 0                                         */
+  double rho, rho_psi;     /* Eq. 12 / Eq. 19 penalty weights, > 0 (G5, G14)             */
+  double w_copy;           /* smoothness weight of the c, s blocks in Q, >= 0 (G10)      */
+  uint32_t boundary_mask;  /* bits x(0), x'(0), x''(0), x(T), x'(T), x''(T); default 0x3F */
+  int32_t alpha_rule;      /* 0: alpha = atan2(yt, xt) (Eq. 21a); 1: atan2(a yt, b xt) (G8) */
+  double res_tol;          /* feasibility threshold tau on r1 for the argmin (G17)       */
+  int32_t device;          /* CUDA device ordinal                                        */
+} bmc_params;
+
+/* One batch (or one shard of a batch) to solve. */
+typedef struct {
+  int64_t B;               /* instances in this call, >= 1                                */
+  int64_t index_base;      /* global index of instance 0 (sharded solves); B+base < 2^30 */
+  int32_t n_obs;           /* obstacles n, 0 <= n <= 160                                  */
+  int32_t iters;           /* AM iterations K >= 0 (K = 0 evaluates the initialisation)  */
+  double bnd[3][6];        /* x, y, psi  x  (p0, v0, a0, pT, vT, aT); selected by the mask */
+  const float* obs_xy;     /* [n][2][q] obstacle centre trajectories x_j(t_k), y_j(t_k)  */
+  const float* obs_ab;     /* [n][2] effective (inflated) semi-axes a_j, b_j > 0 (G13)   */
+  const float* init;       /* [B][3][11] initial Bernstein coefficients c_x, c_y, c_psi  */
+  const float* lambda_in;  /* [B][5][11] warm-start multipliers (lambda, lambda_psi) or NULL */
+} bmc_problem;
+
+/* Outputs.  Layouts are row-major fp32 (int64 for best). */
+typedef struct {
+  float* coeffs;           /* [B][5][11] c_x, c_c, c_y, c_s, c_psi (Bernstein)            */
+  float* lambda_out;       /* [B][5][11] final lambda (4 blocks) and lambda_psi, or NULL */
+  float* residual;         /* [B][2] r1 = ||F xi1 - g||_2, r_psi = ||theta - P xi2||_2   */
+  float* cost;             /* [B] J = sum_t (xdd^2 + ydd^2 + psidd^2)                     */
+  float* res_trace;        /* [B][iters] r1 after every iteration, or NULL               */
+  int64_t* best;           /* [2] {global best index, packed key}:
+                              key = infeasible << 62 | fp32bits(v) << 30 | index,
+                              infeasible = !(r1 <= tau) or non-finite; v = J if feasible
+                              else r1; the minimum key wins (ties -> lowest index) */
+} bmc_result;
+
+/* Build the context: Bernstein basis, boundary rows, per-channel KKT
+ * inverses in fp64 (Eq. 3-4 "constant" inverse).  The device is
+ * params->device.  Returns BMC_EINVAL (bad parameter, message says which),
+ * BMC_ESINGULAR, BMC_ECUDA or BMC_ENOMEM; *out is NULL on error. */
+int32_t bmc_setup(const bmc_params* params, bmc_ctx** out);
+
+/* Device solve, asynchronous on `stream`.  Every pointer in `prob` and `res`
+ * is a caller-owned DEVICE pointer on params.device (contiguous, 16-byte
+ * aligned); the library reads/writes them only during the stream-ordered
+ * execution of this call and never frees or retains them.  The first solve
+ * with a new n_obs builds and uploads that n's constants (synchronous, once).
+ * Errors: BMC_EINVAL (B < 1, n or K out of range, NULL required pointer,
+ * misaligned pointer), BMC_ECUDA (launch failure), BMC_ENOMEM. */
+int32_t bmc_solve(bmc_ctx* ctx, const bmc_problem* prob, const bmc_result* res,
+                  bmc_stream_t stream);
+
+/* End-to-end solve with HOST pointers (pinned memory recommended): copies the
+ * inputs to context-owned device buffers, runs bmc_solve on the context's
+ * stream, copies every non-NULL output back, and synchronises.  Same layouts
+ * and errors as bmc_solve. */
+int32_t bmc_solve_host(bmc_ctx* ctx, const bmc_problem* prob_host, const bmc_result* res_host);
+
+/* Kernel launches issued by the last bmc_solve / bmc_solve_host on ctx. */
+int32_t bmc_last_launch_count(const bmc_ctx* ctx);
+
+/* Release everything owned by the context (NULL is a no-op). */
+void bmc_destroy(bmc_ctx* ctx);
+
+/* Message of the last error on the calling thread ("" if none). */
+const char* bmc_last_error(void);
+
+/* ABI version (major * 100 + minor). */
+int32_t bmc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMC_H */

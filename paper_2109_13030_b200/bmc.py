@@ -1,0 +1,185 @@
+"""Thin ctypes binding of include/bmc.h (argument marshalling only).
+
+Every step of the AM iteration runs in libbmc.so (csrc/bmc_kernel.cuh);
+PyTorch is used here only to allocate device / pinned-host memory and to
+name the current CUDA stream.  There is no CPU fallback: if the library is
+missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIBPATH = os.path.join(_HERE, "libbmc.so")
+NV = 11
+
+BMC_OK, BMC_EINVAL, BMC_ESINGULAR, BMC_ECUDA, BMC_ENOMEM = 0, 1, 2, 3, 4
+_ERRNAMES = {1: "BMC_EINVAL", 2: "BMC_ESINGULAR", 3: "BMC_ECUDA", 4: "BMC_ENOMEM"}
+
+_fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
+
+
+class BmcParams(C.Structure):
+    _fields_ = [("q", C.c_int32), ("T", C.c_double), ("degree", C.c_int32), ("m", C.c_int32),
+                ("r", _dp), ("v_max", C.c_double), ("a_max", C.c_double), ("rho", C.c_double),
+                ("rho_psi", C.c_double), ("w_copy", C.c_double), ("boundary_mask", C.c_uint32),
+                ("alpha_rule", C.c_int32), ("res_tol", C.c_double), ("device", C.c_int32)]
+
+
+class BmcProblem(C.Structure):
+    _fields_ = [("B", C.c_int64), ("index_base", C.c_int64), ("n_obs", C.c_int32),
+                ("iters", C.c_int32), ("bnd", C.c_double * 18), ("obs_xy", C.c_void_p),
+                ("obs_ab", C.c_void_p), ("init", C.c_void_p), ("lambda_in", C.c_void_p)]
+
+
+class BmcResult(C.Structure):
+    _fields_ = [("coeffs", C.c_void_p), ("lambda_out", C.c_void_p), ("residual", C.c_void_p),
+                ("cost", C.c_void_p), ("res_trace", C.c_void_p), ("best", C.c_void_p)]
+
+
+class BmcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library(path: str = LIBPATH):
+    """Load libbmc.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built; run __graft_entry__.build() (make -C csrc)")
+        L = C.CDLL(path)
+        L.bmc_setup.argtypes = [C.POINTER(BmcParams), C.POINTER(C.c_void_p)]
+        L.bmc_setup.restype = C.c_int32
+        L.bmc_solve.argtypes = [C.c_void_p, C.POINTER(BmcProblem), C.POINTER(BmcResult), C.c_void_p]
+        L.bmc_solve.restype = C.c_int32
+        L.bmc_solve_host.argtypes = [C.c_void_p, C.POINTER(BmcProblem), C.POINTER(BmcResult)]
+        L.bmc_solve_host.restype = C.c_int32
+        L.bmc_destroy.argtypes = [C.c_void_p]
+        L.bmc_destroy.restype = None
+        L.bmc_last_error.argtypes = []
+        L.bmc_last_error.restype = C.c_char_p
+        L.bmc_version.restype = C.c_int32
+        L.bmc_last_launch_count.argtypes = [C.c_void_p]
+        L.bmc_last_launch_count.restype = C.c_int32
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != BMC_OK:
+        raise BmcError(rc, load_library().bmc_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+class Solver:
+    """bmc_setup / bmc_solve on one device (Python names mirror the C-ABI)."""
+
+    def __init__(self, q: int, T: float, r: Sequence[float], v_max: float, a_max: float,
+                 rho: float = 1.0, rho_psi: float = 1.0, w_copy: float = 0.0,
+                 boundary_mask: int = 0x3F, alpha_rule: int = 0, res_tol: float = 0.05,
+                 device: Optional[int] = None, degree: int = 10):
+        import torch
+        L = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        self.q, self.m = int(q), len(r)
+        self._r = np.ascontiguousarray(np.asarray(r, dtype=np.float64))
+        self.params = BmcParams(q, T, degree, self.m, self._r.ctypes.data_as(_dp), v_max, a_max,
+                                rho, rho_psi, w_copy, boundary_mask, alpha_rule, res_tol, self.device)
+        h = C.c_void_p()
+        _check(L.bmc_setup(C.byref(self.params), C.byref(h)))
+        self._h = h
+        self.last_launches = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().bmc_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _problem(self, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base):
+        bnd = np.asarray(bnd, dtype=np.float64).reshape(18)
+        return BmcProblem(B, index_base, n, iters, (C.c_double * 18)(*bnd), _ptr(obs_xy),
+                          _ptr(obs_ab), _ptr(init), _ptr(lambda_in))
+
+    def solve(self, init, obs_xy, obs_ab, bnd, iters: int, lambda_in=None, trace: bool = False,
+              index_base: int = 0, out: Optional[dict] = None, stream=None) -> dict:
+        """Device solve on the current (or given) torch stream; returns device tensors."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        B = int(init.shape[0])
+        n = int(obs_xy.shape[0]) if obs_xy is not None else 0
+        for name, t in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
+            if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev):
+                raise ValueError(f"{name} must be a contiguous float32 tensor on {dev}")
+        if out is None:
+            out = dict(
+                coeffs=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
+                lambda_out=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
+                residual=torch.empty((B, 2), dtype=torch.float32, device=dev),
+                cost=torch.empty((B,), dtype=torch.float32, device=dev),
+                best=torch.empty((2,), dtype=torch.int64, device=dev),
+            )
+            if trace and iters > 0:
+                out["res_trace"] = torch.empty((B, iters), dtype=torch.float32, device=dev)
+        prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
+                             lambda_in, index_base)
+        res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
+                        _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        L = load_library()
+        _check(L.bmc_solve(self._h, C.byref(prob), C.byref(res), C.c_void_p(stream.cuda_stream)))
+        self.last_launches = L.bmc_last_launch_count(self._h)
+        return out
+
+    def solve_host(self, init: np.ndarray, obs_xy: np.ndarray, obs_ab: np.ndarray, bnd, iters: int,
+                   lambda_in: Optional[np.ndarray] = None, trace: bool = False, index_base: int = 0,
+                   out: Optional[dict] = None) -> dict:
+        """End-to-end solve from host arrays (pinned recommended); synchronous."""
+        B = int(init.shape[0])
+        n = int(obs_xy.shape[0]) if obs_xy is not None else 0
+        for name, a in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
+            if a is not None and (a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]):
+                raise ValueError(f"{name} must be a C-contiguous float32 array")
+        if out is None:
+            out = dict(coeffs=np.empty((B, 5, NV), np.float32), lambda_out=np.empty((B, 5, NV), np.float32),
+                       residual=np.empty((B, 2), np.float32), cost=np.empty((B,), np.float32),
+                       best=np.empty((2,), np.int64))
+            if trace and iters > 0:
+                out["res_trace"] = np.empty((B, iters), np.float32)
+        prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
+                             lambda_in, index_base)
+        res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
+                        _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+        L = load_library()
+        _check(L.bmc_solve_host(self._h, C.byref(prob), C.byref(res)))
+        self.last_launches = L.bmc_last_launch_count(self._h)
+        return out
+
+
+def solver_for(cfg, device: Optional[int] = None, **kw) -> Solver:
+    """Solver for a synth.Config (q, T, footprint, bounds, weights)."""
+    args = dict(q=cfg.q, T=cfg.T, r=cfg.offsets, v_max=cfg.v_max, a_max=cfg.a_max, rho=cfg.rho,
+                rho_psi=cfg.rho_psi, res_tol=cfg.res_tol, device=device)
+    args.update(kw)
+    return Solver(**args)

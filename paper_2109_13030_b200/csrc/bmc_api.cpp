@@ -1,0 +1,370 @@
+// bmc_api.cpp -- the C-ABI of include/bmc.h: argument validation, the
+// context (host constants, per-n device blobs, argmin workspace), device and
+// host-buffer solves.  No compute happens here beyond the one-off fp64 setup
+// (setup.cpp); every step of the iteration runs in bmc_kernel.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/bmc.h"
+#include "bmc_internal.h"
+
+namespace bmc {
+cudaError_t launch_am(const KernelArgs& a, int wpc, cudaStream_t s);
+size_t kernel_smem_bytes(int QP, int n, int wpc);
+}  // namespace bmc
+
+using namespace bmc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int32_t fail(int32_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int32_t cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? BMC_ENOMEM : BMC_ECUDA;
+}
+
+struct DeviceGuard {  // restore the caller's current device
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct Blob {
+  unsigned char* d = nullptr;
+  int nb = 0;
+};
+
+struct HostBuf {  // context-owned device buffers for bmc_solve_host
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace
+
+struct bmc_ctx {
+  bmc_params p{};
+  std::vector<double> r;
+  int q = 0, QP = 0, NT = 0;
+  std::map<int, Blob> blobs;   // by n_obs
+  unsigned long long* ws_key = nullptr;
+  unsigned int* ws_count = nullptr;
+  cudaStream_t hstream = nullptr;
+  HostBuf hb[10];
+  int32_t last_launches = 0;
+};
+
+extern "C" {
+
+int32_t bmc_version(void) { return 100; }
+
+const char* bmc_last_error(void) { return g_err.c_str(); }
+
+int32_t bmc_last_launch_count(const bmc_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+static int32_t validate_params(const bmc_params* p) {
+  if (!p) return fail(BMC_EINVAL, "params is NULL");
+  if (p->degree != 10) return fail(BMC_EINVAL, "degree must be 10 (n_v = 11)");
+  if (p->q < p->degree + 1) return fail(BMC_EINVAL, "q < degree + 1");
+  if (p->q > Q_MAX) return fail(BMC_EINVAL, "q > 128");
+  if (!(p->T > 0.0) || !std::isfinite(p->T)) return fail(BMC_EINVAL, "T must be > 0");
+  if (p->m < 1 || p->m > M_MAX) return fail(BMC_EINVAL, "m must be in [1, 8]");
+  if (!p->r) return fail(BMC_EINVAL, "r is NULL");
+  for (int i = 0; i < p->m; ++i)
+    if (!std::isfinite(p->r[i])) return fail(BMC_EINVAL, "r has a non-finite entry");
+  if (!(p->v_max > 0.0) || !(p->a_max > 0.0)) return fail(BMC_EINVAL, "v_max and a_max must be > 0");
+  if (!(p->rho > 0.0) || !(p->rho_psi > 0.0)) return fail(BMC_EINVAL, "rho and rho_psi must be > 0");
+  if (!(p->w_copy >= 0.0)) return fail(BMC_EINVAL, "w_copy must be >= 0");
+  if (p->boundary_mask & ~0x3Fu) return fail(BMC_EINVAL, "boundary_mask has bits above 0x3F");
+  if (p->alpha_rule != 0 && p->alpha_rule != 1) return fail(BMC_EINVAL, "alpha_rule must be 0 or 1");
+  if (std::isnan(p->res_tol)) return fail(BMC_EINVAL, "res_tol is NaN");
+  return BMC_OK;
+}
+
+static SetupParams setup_params(const bmc_ctx* c) {
+  SetupParams s;
+  s.q = c->p.q;
+  s.T = c->p.T;
+  s.m = c->p.m;
+  s.r = c->r.data();
+  s.rho = c->p.rho;
+  s.rho_psi = c->p.rho_psi;
+  s.w_copy = c->p.w_copy;
+  s.mask = c->p.boundary_mask;
+  return s;
+}
+
+int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
+  if (!out) return fail(BMC_EINVAL, "out is NULL");
+  *out = nullptr;
+  int32_t rc = validate_params(params);
+  if (rc != BMC_OK) return rc;
+  // singularity of the boundary / KKT does not depend on n: check it now
+  bmc_ctx* c = new (std::nothrow) bmc_ctx();
+  if (!c) return fail(BMC_ENOMEM, "host allocation failed");
+  c->p = *params;
+  c->r.assign(params->r, params->r + params->m);
+  c->p.r = c->r.data();
+  c->q = params->q;
+  c->QP = ((params->q + 31) / 32) * 32;
+  c->NT = c->QP / 32;
+  {
+    HostConsts hc;
+    std::string err;
+    if (build_consts(setup_params(c), 0, &hc, &err) != 0) {
+      delete[] hc.pt;
+      delete c;
+      return fail(BMC_ESINGULAR, err);
+    }
+    delete[] hc.pt;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  if (params->device < 0 || params->device >= ndev) {
+    delete c;
+    return fail(BMC_EINVAL, "device ordinal out of range");
+  }
+  DeviceGuard g(params->device);
+  void* ws = nullptr;
+  e = cudaMalloc(&ws, 16);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(workspace)");
+  }
+  c->ws_key = reinterpret_cast<unsigned long long*>(ws);
+  c->ws_count = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + 8);
+  if ((e = cudaMemset(c->ws_key, 0xFF, 8)) != cudaSuccess || (e = cudaMemset(c->ws_count, 0, 8)) != cudaSuccess) {
+    bmc_destroy(c);
+    return cuda_fail(e, "cudaMemset(workspace)");
+  }
+  *out = c;
+  g_err.clear();
+  return BMC_OK;
+}
+
+void bmc_destroy(bmc_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->p.device);
+  for (auto& kv : c->blobs) cudaFree(kv.second.d);
+  if (c->ws_key) cudaFree(c->ws_key);
+  for (auto& b : c->hb) cudaFree(b.p);
+  if (c->hstream) cudaStreamDestroy(c->hstream);
+  delete c;
+}
+
+static int32_t get_blob(bmc_ctx* c, int n, Blob** out) {
+  auto it = c->blobs.find(n);
+  if (it != c->blobs.end()) {
+    *out = &it->second;
+    return BMC_OK;
+  }
+  HostConsts hc;
+  std::string err;
+  if (build_consts(setup_params(c), n, &hc, &err) != 0) {
+    delete[] hc.pt;
+    return fail(BMC_ESINGULAR, err);
+  }
+  Blob b;
+  b.nb = hc.nb;
+  const size_t bytes = BlobLayout::bytes(hc.QP);
+  cudaError_t e = cudaMalloc(&b.d, bytes);
+  if (e != cudaSuccess) {
+    delete[] hc.pt;
+    return cuda_fail(e, "cudaMalloc(blob)");
+  }
+  std::vector<unsigned char> host(bytes);
+  std::memcpy(host.data(), hc.blob_f64, BlobLayout::bytes_f64);
+  std::memcpy(host.data() + BlobLayout::bytes_f64, hc.pt, BlobLayout::bytes_f32(hc.QP));
+  delete[] hc.pt;
+  e = cudaMemcpy(b.d, host.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(b.d);
+    return cuda_fail(e, "cudaMemcpy(blob)");
+  }
+  c->blobs[n] = b;
+  *out = &c->blobs[n];
+  return BMC_OK;
+}
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static int32_t validate_problem(const bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs) {
+  if (!c) return fail(BMC_EINVAL, "ctx is NULL");
+  if (!pr || !rs) return fail(BMC_EINVAL, "problem or result is NULL");
+  if (pr->B < 1) return fail(BMC_EINVAL, "B must be >= 1");
+  if (pr->index_base < 0 || pr->B + pr->index_base > (1ll << 30))
+    return fail(BMC_EINVAL, "index_base + B must be in [1, 2^30]");
+  if (pr->n_obs < 0 || pr->n_obs > N_MAX) return fail(BMC_EINVAL, "n_obs must be in [0, 160]");
+  if (pr->iters < 0) return fail(BMC_EINVAL, "iters must be >= 0");
+  if (pr->n_obs > 0 && (!pr->obs_xy || !pr->obs_ab)) return fail(BMC_EINVAL, "obs_xy / obs_ab is NULL");
+  if (!pr->init) return fail(BMC_EINVAL, "init is NULL");
+  if (!rs->coeffs || !rs->residual || !rs->cost || !rs->best)
+    return fail(BMC_EINVAL, "coeffs, residual, cost and best are required");
+  const void* f32[] = {pr->obs_xy, pr->obs_ab, pr->init, pr->lambda_in, rs->coeffs,
+                       rs->lambda_out, rs->residual, rs->cost, rs->res_trace};
+  for (const void* p : f32)
+    if (p && !aligned(p, 4)) return fail(BMC_EINVAL, "misaligned fp32 pointer");
+  if (!aligned(rs->best, 8)) return fail(BMC_EINVAL, "misaligned best pointer");
+  for (int ch = 0; ch < 3; ++ch)
+    for (int j = 0; j < 6; ++j)
+      if (!std::isfinite(pr->bnd[ch][j])) return fail(BMC_EINVAL, "bnd has a non-finite entry");
+  return BMC_OK;
+}
+
+static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, cudaStream_t s) {
+  Blob* blob = nullptr;
+  int32_t rc = get_blob(c, pr->n_obs, &blob);
+  if (rc != BMC_OK) return rc;
+  int wpc = 4;
+  while (wpc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, wpc) > 227 * 1024) --wpc;
+  if (kernel_smem_bytes(c->QP, pr->n_obs, wpc) > 227 * 1024)
+    return fail(BMC_EINVAL, "n_obs * q too large for shared memory");
+  KernelArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.blob = blob->d;
+  a.obs_xy = pr->obs_xy;
+  a.obs_ab = pr->obs_ab;
+  a.init = pr->init;
+  a.lambda_in = pr->lambda_in;
+  a.coeffs = rs->coeffs;
+  a.lambda_out = rs->lambda_out;
+  a.residual = rs->residual;
+  a.cost = rs->cost;
+  a.res_trace = (pr->iters > 0) ? rs->res_trace : nullptr;
+  a.best = reinterpret_cast<long long*>(rs->best);
+  a.ws_key = c->ws_key;
+  a.ws_count = c->ws_count;
+  a.B = pr->B;
+  a.index_base = pr->index_base;
+  a.q = c->q;
+  a.QP = c->QP;
+  a.NT = c->NT;
+  a.n = pr->n_obs;
+  a.m = c->p.m;
+  a.nb = blob->nb;
+  a.iters = pr->iters;
+  a.alpha_rule = c->p.alpha_rule;
+  double R1 = 0.0, R2 = 0.0;
+  for (int i = 0; i < c->p.m; ++i) {
+    a.r[i] = (float)c->r[i];
+    R1 += c->r[i];
+    R2 += c->r[i] * c->r[i];
+  }
+  a.nR1 = (float)(pr->n_obs * R1);
+  a.nR2p1 = (float)(pr->n_obs * R2 + 1.0);
+  a.v_max = (float)c->p.v_max;
+  a.a_max = (float)c->p.a_max;
+  a.rho = c->p.rho;
+  a.rho_psi = c->p.rho_psi;
+  a.res_tol = c->p.res_tol;
+  int r = 0;
+  for (int bit = 0; bit < 6; ++bit) {
+    if (!(c->p.boundary_mask & (1u << bit))) continue;
+    for (int ch = 0; ch < 3; ++ch) a.b[ch][r] = pr->bnd[ch][bit];
+    ++r;
+  }
+  cudaError_t e = launch_am(a, wpc, s);
+  c->last_launches = 1;
+  if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");
+  return BMC_OK;
+}
+
+int32_t bmc_solve(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, bmc_stream_t stream) {
+  int32_t rc = validate_problem(c, pr, rs);
+  if (rc != BMC_OK) return rc;
+  DeviceGuard g(c->p.device);
+  c->last_launches = 0;
+  rc = solve_impl(c, pr, rs, reinterpret_cast<cudaStream_t>(stream));
+  if (rc == BMC_OK) g_err.clear();
+  return rc;
+}
+
+static int32_t ensure(bmc_ctx* c, int slot, size_t bytes, void** out) {
+  HostBuf& b = c->hb[slot];
+  if (b.cap < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes < 256 ? 256 : bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(host-solve buffer)");
+    b.cap = bytes < 256 ? 256 : bytes;
+  }
+  *out = b.p;
+  return BMC_OK;
+}
+
+int32_t bmc_solve_host(bmc_ctx* c, const bmc_problem* ph, const bmc_result* rh) {
+  int32_t rc = validate_problem(c, ph, rh);
+  if (rc != BMC_OK) return rc;
+  DeviceGuard g(c->p.device);
+  c->last_launches = 0;
+  cudaError_t e;
+  if (!c->hstream && (e = cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamCreate");
+  const size_t B = (size_t)ph->B, n = (size_t)ph->n_obs, q = (size_t)c->q, K = (size_t)ph->iters;
+  const size_t sz[10] = {n * 2 * q * 4, n * 2 * 4, B * 33 * 4, B * 55 * 4, B * 55 * 4,
+                         B * 55 * 4, B * 2 * 4, B * 4, B * (K ? K : 1) * 4, 16};
+  void* d[10];
+  for (int i = 0; i < 10; ++i)
+    if ((rc = ensure(c, i, sz[i], &d[i])) != BMC_OK) return rc;
+  bmc_problem pd = *ph;
+  bmc_result rd;
+  pd.obs_xy = n ? (const float*)d[0] : nullptr;
+  pd.obs_ab = n ? (const float*)d[1] : nullptr;
+  pd.init = (const float*)d[2];
+  pd.lambda_in = ph->lambda_in ? (const float*)d[3] : nullptr;
+  rd.coeffs = (float*)d[4];
+  rd.lambda_out = rh->lambda_out ? (float*)d[5] : nullptr;
+  rd.residual = (float*)d[6];
+  rd.cost = (float*)d[7];
+  rd.res_trace = rh->res_trace ? (float*)d[8] : nullptr;
+  rd.best = (int64_t*)d[9];
+  cudaStream_t s = c->hstream;
+#define H2D(dst, src, bytes) \
+  if ((bytes) && (e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D")
+#define D2H(dst, src, bytes) \
+  if ((bytes) && (e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return cuda_fail(e, "D2H")
+  if (n) {
+    H2D(d[0], ph->obs_xy, sz[0]);
+    H2D(d[1], ph->obs_ab, sz[1]);
+  }
+  H2D(d[2], ph->init, sz[2]);
+  if (ph->lambda_in) H2D(d[3], ph->lambda_in, sz[3]);
+  rc = solve_impl(c, &pd, &rd, s);
+  if (rc != BMC_OK) return rc;
+  D2H(rh->coeffs, d[4], sz[4]);
+  if (rh->lambda_out) D2H(rh->lambda_out, d[5], sz[5]);
+  D2H(rh->residual, d[6], sz[6]);
+  D2H(rh->cost, d[7], sz[7]);
+  const size_t trace_bytes = rh->res_trace ? B * K * 4 : 0;
+  D2H(rh->res_trace, d[8], trace_bytes);
+  D2H(rh->best, d[9], 16);
+#undef H2D
+#undef D2H
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  g_err.clear();
+  return BMC_OK;
+}
+
+}  // extern "C"

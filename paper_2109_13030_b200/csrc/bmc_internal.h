@@ -1,0 +1,88 @@
+// bmc_internal.h -- shared between the host setup (setup.cpp), the C-ABI
+// (bmc_api.cpp) and the fused kernel (bmc_kernel.cu).  Product path only.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#ifdef __CUDACC__
+#define BMC_HD __host__ __device__
+#else
+#define BMC_HD
+#endif
+
+namespace bmc {
+
+constexpr int NV = 11;        // Bernstein degree 10 (n_v = 11, G12)
+constexpr int NV2 = 2 * NV;   // per-channel xi1 block (pos, copy)
+constexpr int NB_MAX = 6;     // boundary rows per channel (G11)
+constexpr int M_MAX = 8;      // footprint circles
+constexpr int Q_MAX = 128;    // time samples (4 rounds of 32 lanes)
+constexpr int N_MAX = 160;    // obstacles staged in shared memory
+
+// Device constant blob, one per obstacle count n (Q_bar = Q + rho F^T F
+// depends on n through F^T F).  fp64 part first, then fp32 basis.
+// All matrices are stored TRANSPOSED ("[j][k]": element (row k, col j) at
+// j*ld + k) so lane k of a warp reads row k of a mat-vec at consecutive
+// addresses.
+struct BlobLayout {
+  // fp64 section (offsets in doubles)
+  static constexpr int Mt = 0;                 // [22][22] (rho K11 F^T F)^T
+  static constexpr int K11t = Mt + NV2 * NV2;  // [22][22] K11^T
+  static constexpr int K12t = K11t + NV2 * NV2;   // [6][22]  K12^T (rows >= nb zero)
+  static constexpr int Kp11t = K12t + NB_MAX * NV2;  // [11][11]
+  static constexpr int Kp12t = Kp11t + NV * NV;      // [6][11]
+  static constexpr int Gppt = Kp12t + NB_MAX * NV;   // [11][11] rho_psi P^T P
+  static constexpr int Gdd = Gppt + NV * NV;         // [11][11] Pdd^T Pdd (cost)
+  static constexpr int n_doubles_raw = Gdd + NV * NV;
+  static constexpr int n_doubles = (n_doubles_raw + 1) & ~1;   // 16-byte multiple
+  static constexpr size_t bytes_f64 = sizeof(double) * n_doubles;
+  // fp32 section: Pt[3][11][QP] = P, Pdot, Pddot transposed, zero for t >= q
+  BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * 3 * NV * (size_t)QP; }
+  BMC_HD static size_t bytes(int QP) { return bytes_f64 + bytes_f32(QP); }
+};
+
+// Kernel arguments (passed by value).
+struct KernelArgs {
+  const unsigned char* blob;   // device constant blob for this n
+  const float* obs_xy;         // [n][2][q]
+  const float* obs_ab;         // [n][2]
+  const float* init;           // [B][3][11]
+  const float* lambda_in;      // [B][5][11] or null
+  float* coeffs;               // [B][5][11]
+  float* lambda_out;           // [B][5][11] or null
+  float* residual;             // [B][2]
+  float* cost;                 // [B]
+  float* res_trace;            // [B][K] or null
+  long long* best;             // [2]
+  unsigned long long* ws_key;  // argmin workspace (reset by the last CTA)
+  unsigned int* ws_count;
+  long long B, index_base;
+  int q, QP, NT, n, m, nb, iters, alpha_rule;
+  float r[M_MAX];
+  float nR1, nR2p1;            // n sum r_i, n sum r_i^2 + 1 (F^T F closed form)
+  float v_max, a_max;
+  double rho, rho_psi, res_tol;
+  double b[3][NB_MAX];         // selected boundary values: x, y, psi
+};
+
+struct SetupParams {
+  int q;
+  double T;
+  int m;
+  const double* r;
+  double rho, rho_psi, w_copy;
+  unsigned mask;
+};
+
+// host-side constants for one (params, n)
+struct HostConsts {
+  int q, QP, nb, n, m;
+  double blob_f64[BlobLayout::n_doubles];
+  float* pt = nullptr;   // [3][11][QP]
+};
+
+// setup.cpp: fp64 constants for obstacle count n; 0 or 2 (singular) with *err.
+int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err);
+
+}  // namespace bmc

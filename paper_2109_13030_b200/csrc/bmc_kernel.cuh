@@ -1,0 +1,590 @@
+// bmc_kernel.cuh -- fused batched AM iteration of arXiv 2109.13030 on sm_100a.
+//
+// One warp owns one batch instance l for all K iterations (instances are
+// independent, "each instance in the batch is independent"); a CTA of
+// WPC warps shares one shared-memory copy of the batch-invariant data: the
+// basis P, Pdot, Pddot, the KKT inverses (bulk-copied by TMA, cp.async.bulk)
+// and the obstacle trajectories.  Lanes own time samples t = lane + 32 u.
+//
+// Per iteration (paper step order):
+//   A  xi1 step (Eq. 13/17 via Eq. 4):  xi1' = M xi1 + K11 (lambda - rho h) + K12 b
+//      in fp64 (lanes k < 22 own row k of both channels);
+//   B  c, s = P c_c, P c_s; theta = atan2(s, c); P^T theta (warp transpose-reduce);
+//   C  xi2 step (Eq. 19) and lambda_psi (Eq. 23b, G4) in fp64 (lanes k < 11);
+//   D  x, xdot, xddot, y, ..., psi at the lane's t; velocity / acceleration
+//      projections (Eq. 21b-c, 22b-c: projection onto the v_max / a_max disk);
+//      collision projections over all (j, i) (Eq. 21a, 22a) reduced in
+//      registers to D = sum_ij delta_ij and E = sum_i r_i sum_j delta_ij,
+//      delta_ij = (a d cos(alpha), b d sin(alpha)) - (x~, y~), then the
+//      contraction h = F^T (F xi1 - g) (Eq. 10-11 closed form):
+//        h_pos  = P^T (n R1 e - D) - Pd^T dv - Pdd^T da,
+//        h_copy = P^T ((n R2 + 1) e - E),      e = c - cos(psi)  (G9)
+//   E  lambda <- lambda - rho h (Eq. 23a with F^T, G3).
+// The residual r1 = ||F xi1 - g|| is accumulated in the last iteration (or
+// every iteration in trace mode) from the same per-row quantities.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "bmc_internal.h"
+
+#pragma once
+
+namespace bmc {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct WarpSmem {
+  double xi1[2 * NV2];  // [k][ch]
+  double rhs[2 * NV2];  // [k][ch]
+  double xi2[12];
+  double rhsp[12];
+  float cf[5][12];      // fp32 copies of c_x, c_c, c_y, c_s, c_psi (padded)
+  float h[48];
+  float pth[16];
+};
+static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
+
+constexpr int U_DOUBLES = 56;  // u_x[22], u_y[22], u_psi[11] (+pad)
+
+__host__ __device__ inline size_t smem_bytes(int QP, int n, int wpc) {
+  return BlobLayout::bytes(QP) + (size_t)n * QP * sizeof(float2) + (size_t)n * sizeof(float4) +
+         U_DOUBLES * sizeof(double) + (size_t)wpc * sizeof(WarpSmem) + 16;
+}
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+// ------------------------------------------------------------ warp reductions
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// One butterfly stage of the transpose-reduce: CNT values -> CNT/2 values.
+template <int CNT>
+__device__ __forceinline__ void tr_stage(float* v, int off, bool upper) {
+#pragma unroll
+  for (int i = 0; i < CNT / 2; ++i) {
+    const float send = upper ? v[i] : v[i + CNT / 2];
+    const float keep = upper ? v[i + CNT / 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, off);
+  }
+}
+// 32 values per lane -> lane l holds the warp total of value l.
+__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
+  tr_stage<32>(v, 16, lane & 16);
+  tr_stage<16>(v, 8, lane & 8);
+  tr_stage<8>(v, 4, lane & 4);
+  tr_stage<4>(v, 2, lane & 2);
+  tr_stage<2>(v, 1, lane & 1);
+  return v[0];
+}
+// 16 values per lane -> lane l holds the warp total of value l >> 1.
+__device__ __forceinline__ float transpose_reduce16(float* v, int lane) {
+  tr_stage<16>(v, 16, lane & 16);
+  tr_stage<8>(v, 8, lane & 8);
+  tr_stage<4>(v, 4, lane & 4);
+  tr_stage<2>(v, 2, lane & 2);
+  return v[0] + __shfl_xor_sync(FULL, v[0], 1);
+}
+
+__device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
+  const float4 a = reinterpret_cast<const float4*>(src)[0];
+  const float4 b = reinterpret_cast<const float4*>(src)[1];
+  const float4 d = reinterpret_cast<const float4*>(src)[2];
+  c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+  c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  c[8] = d.x; c[9] = d.y; c[10] = d.z;
+}
+
+// --------------------------------------------------- collision projections
+// For every obstacle j and circle i at the lane's t: x~ = X_i - x_j,
+// y~ = Y_i - y_j (X_i = x + r_i cos psi, G9), and the closed-form offset
+// delta = (a d cos(alpha), b d sin(alpha)) - (x~, y~) of Eq. 21a/22a:
+//   kind 0 (a == b, either rule):  delta = (x~, y~) max(a / |(x~,y~)| - 1, 0)
+//   kind 1 (literal atan2(y~,x~)): delta = (x~ (a f - 1), y~ (b f - 1)),
+//                                  f = max(1/rho, (a x~^2 + b y~^2)/(a^2 x~^2 + b^2 y~^2))
+//   kind 2 (scaled, G8):           delta = (x~, y~) max(ab / sqrt(b^2 x~^2 + a^2 y~^2) - 1, 0)
+// GUARD handles x~ = y~ = 0 exactly (G18: alpha = 0, d = 1 -> delta = (a, 0)).
+template <int M, bool RES, bool GUARD>
+__device__ __forceinline__ void coll_loop(const float2* __restrict__ ob, const float4* __restrict__ abi,
+                                          int n, int QP, const float (&X)[M], const float (&Y)[M],
+                                          const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
+                                          float (&Dy)[M], float& rc) {
+#pragma unroll 2
+  for (int j = 0; j < n; ++j) {
+    const float2 o = ob[(size_t)j * QP];
+    const float4 ab = abi[j];
+    if (ab.w == 0.f) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const float xt = X[i] - o.x, yt = Y[i] - o.y;
+        const float r2 = fmaf(yt, yt, xt * xt);
+        const float sc = fmaxf(fmaf(ab.x, rsqrtf(r2), -1.f), 0.f);
+        if (!RES && !GUARD) {
+          Dx[i] = fmaf(sc, xt, Dx[i]);
+          Dy[i] = fmaf(sc, yt, Dy[i]);
+        } else {
+          float dx = sc * xt, dy = sc * yt;
+          if (GUARD && r2 == 0.f) { dx = ab.x; dy = 0.f; }
+          Dx[i] += dx;
+          Dy[i] += dy;
+          if (RES) {
+            const float tx = rec[i] - dx, ty = res_s[i] - dy;
+            rc = fmaf(tx, tx, rc);
+            rc = fmaf(ty, ty, rc);
+          }
+        }
+      }
+    } else {
+      const float a = ab.x, b = ab.y;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const float xt = X[i] - o.x, yt = Y[i] - o.y;
+        const float x2 = xt * xt, y2 = yt * yt;
+        float dx, dy;
+        if (ab.w == 1.f) {
+          const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
+          const float f = fmaxf(rsqrtf(x2 + y2), __fdividef(N, D));
+          dx = xt * fmaf(a, f, -1.f);
+          dy = yt * fmaf(b, f, -1.f);
+        } else {
+          const float R2 = fmaf(a * a, y2, b * b * x2);
+          const float sc = fmaxf(fmaf(ab.z, rsqrtf(R2), -1.f), 0.f);
+          dx = sc * xt;
+          dy = sc * yt;
+        }
+        if (GUARD && x2 + y2 == 0.f) { dx = a; dy = 0.f; }
+        Dx[i] += dx;
+        Dy[i] += dy;
+        if (RES) {
+          const float tx = rec[i] - dx, ty = res_s[i] - dy;
+          rc = fmaf(tx, tx, rc);
+          rc = fmaf(ty, ty, rc);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- phase B
+// c, s at the lane's samples, theta = atan2(s, c) (Eq. 19; G18), and
+// the warp total of P^T theta written to ws->pth[0..10].
+template <int NT>
+__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, int QP, WarpSmem* ws, int lane,
+                                            float (&cr)[NT], float (&sr)[NT], float (&th)[NT]) {
+  float cc[NV], cs[NV];
+  load12(ws->cf[1], cc);
+  load12(ws->cf[3], cs);
+  float acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int t = lane + 32 * u;
+    float p[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
+    float c = 0.f, s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      c = fmaf(p[k], cc[k], c);
+      s = fmaf(p[k], cs[k], s);
+    }
+    const float tht = (c == 0.f && s == 0.f) ? 0.f : atan2f(s, c);
+    cr[u] = c;
+    sr[u] = s;
+    th[u] = tht;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = fmaf(p[k], tht, acc[k]);
+  }
+  const float v = transpose_reduce16(acc, lane);
+  if (!(lane & 1) && (lane >> 1) < NV) ws->pth[lane >> 1] = v;
+}
+
+// ---------------------------------------------------------------- phase D
+template <int NT, int M, bool RES>
+__device__ __forceinline__ void phase_project(const KernelArgs& a, const float* __restrict__ Pt,
+                                              const float2* __restrict__ obs, const float4* __restrict__ abi,
+                                              WarpSmem* ws, int lane, const float (&cr)[NT],
+                                              const float (&sr)[NT], const float (&th)[NT], float& res_out,
+                                              float& rpsi_out) {
+  const int QP = a.QP, q = a.q, n = a.n;
+  float acc[48];
+#pragma unroll
+  for (int k = 0; k < 48; ++k) acc[k] = 0.f;
+  float res = 0.f, rps = 0.f;
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int t = lane + 32 * u;
+    float x = 0.f, y = 0.f, xd = 0.f, yd = 0.f, xdd = 0.f, ydd = 0.f, psi = 0.f;
+    {
+      float cx[NV], cy[NV], cp[NV];
+      load12(ws->cf[0], cx);
+      load12(ws->cf[2], cy);
+      load12(ws->cf[4], cp);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const float p = Pt[k * QP + t];
+        x = fmaf(p, cx[k], x);
+        y = fmaf(p, cy[k], y);
+        psi = fmaf(p, cp[k], psi);
+      }
+      float pd[NV], pdd[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        pd[k] = Pt[(NV + k) * QP + t];
+        pdd[k] = Pt[(2 * NV + k) * QP + t];
+        xd = fmaf(pd[k], cx[k], xd);
+        yd = fmaf(pd[k], cy[k], yd);
+        xdd = fmaf(pdd[k], cx[k], xdd);
+        ydd = fmaf(pdd[k], cy[k], ydd);
+      }
+      // velocity / acceleration: g = projection onto the bound disk (G6, G7)
+      const float sv = fminf(fmaf(a.v_max, rsqrtf(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
+      const float sa = fminf(fmaf(a.a_max, rsqrtf(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
+      const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        acc[k] = fmaf(pd[k], -dvx, fmaf(pdd[k], -dax, acc[k]));
+        acc[NV2 + k] = fmaf(pd[k], -dvy, fmaf(pdd[k], -day, acc[NV2 + k]));
+      }
+      if (RES && t < q) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
+    }
+    float sp, cps;
+    sincosf(psi, &sp, &cps);
+    const float ec = cr[u] - cps, es = sr[u] - sp;
+    float X[M], Y[M], Dx[M], Dy[M], rec[M], res_s[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      X[i] = fmaf(a.r[i], cps, x);
+      Y[i] = fmaf(a.r[i], sp, y);
+      Dx[i] = 0.f;
+      Dy[i] = 0.f;
+      rec[i] = a.r[i] * ec;
+      res_s[i] = a.r[i] * es;
+    }
+    float rc = 0.f;
+    coll_loop<M, RES, false>(obs + t, abi, n, QP, X, Y, rec, res_s, Dx, Dy, rc);
+    float chk = rc;
+#pragma unroll
+    for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
+    if (__any_sync(FULL, !isfinite(chk))) {   // rare: x~ = y~ = 0 exactly (G18)
+#pragma unroll
+      for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
+      rc = 0.f;
+      coll_loop<M, RES, true>(obs + t, abi, n, QP, X, Y, rec, res_s, Dx, Dy, rc);
+    }
+    float Ds_x = 0.f, Ds_y = 0.f, Ex = 0.f, Ey = 0.f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      Ds_x += Dx[i];
+      Ds_y += Dy[i];
+      Ex = fmaf(a.r[i], Dx[i], Ex);
+      Ey = fmaf(a.r[i], Dy[i], Ey);
+    }
+    const float u1x = fmaf(a.nR1, ec, -Ds_x), u1y = fmaf(a.nR1, es, -Ds_y);
+    const float vx = fmaf(a.nR2p1, ec, -Ex), vy = fmaf(a.nR2p1, es, -Ey);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const float p = Pt[k * QP + t];
+      acc[k] = fmaf(p, u1x, acc[k]);
+      acc[NV + k] = fmaf(p, vx, acc[NV + k]);
+      acc[NV2 + k] = fmaf(p, u1y, acc[NV2 + k]);
+      acc[NV2 + NV + k] = fmaf(p, vy, acc[NV2 + NV + k]);
+    }
+    if (t < q) {
+      if (RES) res += rc + ec * ec + es * es;
+      rps = fmaf(th[u] - psi, th[u] - psi, rps);
+    }
+  }
+  const float v32 = transpose_reduce32(acc, lane);
+  const float v16 = transpose_reduce16(acc + 32, lane);
+  ws->h[lane] = v32;
+  if (!(lane & 1)) ws->h[32 + (lane >> 1)] = v16;
+  if (RES) {
+    res_out = warp_sum(res);
+    rpsi_out = warp_sum(rps);
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <int NT, int M>
+__global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
+  const int QP = a.QP, n = a.n, q = a.q, K = a.iters;
+  const double* sf = reinterpret_cast<const double*>(smem);
+  const float* Pt = reinterpret_cast<const float*>(smem + BlobLayout::bytes_f64);
+  float2* obs = reinterpret_cast<float2*>(smem + BlobLayout::bytes(QP));
+  float4* abi = reinterpret_cast<float4*>(obs + (size_t)n * QP);
+  double* ub = reinterpret_cast<double*>(abi + n);
+  WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
+  WarpSmem* ws = wsbase + warp;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wsbase + wpc);
+
+  // --- stage the batch-invariant data -------------------------------------
+  if (tid == 0) mbar_init(mbar, 1);
+  __syncthreads();
+  const unsigned blob_bytes = (unsigned)BlobLayout::bytes(QP);
+  if (tid == 0) {
+    mbar_arrive_expect_tx(mbar, blob_bytes);
+    constexpr unsigned CHUNK = 16384;
+    for (unsigned off = 0; off < blob_bytes; off += CHUNK) {
+      const unsigned nbytes = (blob_bytes - off < CHUNK) ? (blob_bytes - off) : CHUNK;
+      bulk_g2s(smem + off, a.blob + off, nbytes, mbar);
+    }
+  }
+  for (int idx = tid; idx < n * QP; idx += blockDim.x) {
+    const int j = idx / QP, t = idx - j * QP;
+    float2 v = make_float2(1.0e4f, 1.0e4f);   // padding samples: far away, delta = 0
+    if (t < q) v = make_float2(__ldg(a.obs_xy + (size_t)(2 * j) * q + t), __ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t));
+    obs[idx] = v;
+  }
+  for (int j = tid; j < n; j += blockDim.x) {
+    const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
+    const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
+    abi[j] = make_float4(aa, bb, aa * bb, kind);
+  }
+  for (int i = tid; i < wpc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
+  mbar_wait(mbar, 0);
+  __syncthreads();
+  if (tid < NV2) {   // u = K12 b per channel (boundary part of Eq. 4)
+    double sx = 0.0, sy = 0.0;
+    for (int r = 0; r < a.nb; ++r) {
+      sx = fma(sf[BlobLayout::K12t + r * NV2 + tid], a.b[0][r], sx);
+      sy = fma(sf[BlobLayout::K12t + r * NV2 + tid], a.b[1][r], sy);
+    }
+    ub[tid] = sx;
+    ub[NV2 + tid] = sy;
+    if (tid < NV) {
+      double s = 0.0;
+      for (int r = 0; r < a.nb; ++r) s = fma(sf[BlobLayout::Kp12t + r * NV + tid], a.b[2][r], s);
+      ub[2 * NV2 + tid] = s;
+    }
+  }
+  __syncthreads();
+
+  const long long l = (long long)blockIdx.x * wpc + warp;
+  if (l < a.B) {
+    const int k = lane;
+    const double rho = a.rho, rho_psi = a.rho_psi;
+    double xiX = 0.0, xiY = 0.0, lamX = 0.0, lamY = 0.0, xi2r = 0.0, lamp = 0.0;
+    const float* ini = a.init + l * 3 * NV;
+    if (k < NV) {   // step 1: xi2 from the input, copies start at 0 (G15)
+      xiX = ini[k];
+      xiY = ini[NV + k];
+      xi2r = ini[2 * NV + k];
+    }
+    if (a.lambda_in) {
+      const float* li = a.lambda_in + l * 5 * NV;
+      if (k < NV2) { lamX = li[k]; lamY = li[NV2 + k]; }
+      if (k < NV) lamp = li[2 * NV2 + k];
+    }
+    auto publish_xi1 = [&]() {
+      if (k < NV) { ws->cf[0][k] = (float)xiX; ws->cf[2][k] = (float)xiY; }
+      else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
+      if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
+    };
+    publish_xi1();
+    if (k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
+    __syncwarp();
+
+    float cr[NT], sr[NT], th[NT];
+    float r1sq = 0.f, rpsq = 0.f;
+    const bool trace = a.res_trace != nullptr;
+    // initialisation of xi3, xi4 / g on the initial trajectory (G15)
+    phase_theta<NT>(Pt, QP, ws, lane, cr, sr, th);
+    if (K == 0) phase_project<NT, M, true>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+    else phase_project<NT, M, false>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+    __syncwarp();
+
+    for (int it = 0; it < K; ++it) {
+      // ---- A: xi1 step -----------------------------------------------------
+      if (k < NV2) {
+        ws->rhs[2 * k] = lamX - rho * (double)ws->h[k];
+        ws->rhs[2 * k + 1] = lamY - rho * (double)ws->h[NV2 + k];
+      }
+      __syncwarp();
+      if (k < NV2) {
+        double ax = ub[k], ay = ub[NV2 + k], bx = 0.0, by = 0.0;
+#pragma unroll 11
+        for (int j = 0; j < NV2; ++j) {
+          const double mkj = sf[BlobLayout::Mt + j * NV2 + k];
+          const double kkj = sf[BlobLayout::K11t + j * NV2 + k];
+          const double2 xj = reinterpret_cast<const double2*>(ws->xi1)[j];
+          const double2 rj = reinterpret_cast<const double2*>(ws->rhs)[j];
+          ax = fma(mkj, xj.x, ax);
+          ay = fma(mkj, xj.y, ay);
+          bx = fma(kkj, rj.x, bx);
+          by = fma(kkj, rj.y, by);
+        }
+        xiX = ax + bx;
+        xiY = ay + by;
+      }
+      __syncwarp();
+      publish_xi1();
+      __syncwarp();
+      // ---- B: heading target ----------------------------------------------
+      phase_theta<NT>(Pt, QP, ws, lane, cr, sr, th);
+      __syncwarp();
+      // ---- C: xi2 step + lambda_psi ------------------------------------------
+      if (k < NV) ws->rhsp[k] = lamp + rho_psi * (double)ws->pth[k];
+      __syncwarp();
+      if (k < NV) {
+        double s = ub[2 * NV2 + k];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) s = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhsp[j], s);
+        xi2r = s;
+        ws->xi2[k] = s;
+        ws->cf[4][k] = (float)s;
+      }
+      __syncwarp();
+      if (k < NV) {
+        double gs = 0.0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) gs = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2[j], gs);
+        lamp -= gs - rho_psi * (double)ws->pth[k];
+      }
+      // ---- D: projections + contraction -------------------------------------
+      const bool want_res = trace || (it == K - 1);
+      if (want_res) phase_project<NT, M, true>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+      else phase_project<NT, M, false>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+      __syncwarp();
+      // ---- E: multipliers ------------------------------------------------------
+      if (k < NV2) {
+        lamX -= rho * (double)ws->h[k];
+        lamY -= rho * (double)ws->h[NV2 + k];
+      }
+      if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(r1sq);
+    }
+
+    // ---- outputs ------------------------------------------------------------
+    double jpart = 0.0;
+    if (k < NV) {   // J = sum_ch c^T (Pdd^T Pdd) c, fp64 (Eq. 1a, G17)
+      double gx = 0.0, gy = 0.0, gp = 0.0;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const double g = sf[BlobLayout::Gdd + j * NV + k];
+        gx = fma(g, ws->xi1[2 * j], gx);
+        gy = fma(g, ws->xi1[2 * j + 1], gy);
+        gp = fma(g, ws->xi2[j], gp);
+      }
+      jpart = gx * xiX + gy * xiY + gp * xi2r;
+    }
+    const double J = warp_sum(jpart);
+    float* co = a.coeffs + l * 5 * NV;
+    if (k < NV2) { co[k] = (float)xiX; co[NV2 + k] = (float)xiY; }
+    if (k < NV) co[2 * NV2 + k] = (float)xi2r;
+    if (a.lambda_out) {
+      float* lo = a.lambda_out + l * 5 * NV;
+      if (k < NV2) { lo[k] = (float)lamX; lo[NV2 + k] = (float)lamY; }
+      if (k < NV) lo[2 * NV2 + k] = (float)lamp;
+    }
+    if (lane == 0) {
+      const float r1 = sqrtf(r1sq), rp = sqrtf(rpsq);
+      a.residual[2 * l] = r1;
+      a.residual[2 * l + 1] = rp;
+      a.cost[l] = (float)J;
+      // packed argmin key (G17): infeasible << 62 | fp32 bits(value) << 30 | index
+      unsigned long long infeasible = !((double)r1 <= a.res_tol);
+      const double v = infeasible ? (double)r1 : J;
+      const float vf = __double2float_rn(v);
+      unsigned bits;
+      if (!isfinite(v) || !isfinite(vf) || !isfinite(J) || !isfinite(r1)) {
+        infeasible = 1;
+        bits = 0x7F800000u;
+      } else {
+        bits = __float_as_uint(vf > 0.f ? vf : 0.f);
+      }
+      const unsigned long long gidx = (unsigned long long)(a.index_base + l) & ((1ull << 30) - 1);
+      const unsigned long long key = (infeasible << 62) | ((unsigned long long)bits << 30) | gidx;
+      atomicMin(a.ws_key, key);
+      __threadfence();
+    }
+  }
+  // ---- grid-wide argmin: the last CTA publishes and resets the workspace ----
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned ticket = atomicAdd(a.ws_count, 1u);
+    if (ticket == gridDim.x - 1) {
+      __threadfence();
+      const unsigned long long key = atomicExch(a.ws_key, ~0ull);
+      a.best[0] = (long long)(key & ((1ull << 30) - 1));
+      a.best[1] = (long long)key;
+      atomicExch(a.ws_count, 0u);
+    }
+  }
+}
+
+template <int NT, int M>
+cudaError_t launch_t(const KernelArgs& a, int wpc, size_t smem, cudaStream_t s) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<NT, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const unsigned grid = (unsigned)((a.B + wpc - 1) / wpc);
+  bmc_am_kernel<NT, M><<<grid, 32 * wpc, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t kernel_smem_bytes(int QP, int n, int wpc);
+
+// One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
+// this; bmc_launch.cu dispatches on m.
+template <int M>
+cudaError_t launch_am_m(const KernelArgs& a, int wpc, cudaStream_t s) {
+  const size_t smem = smem_bytes(a.QP, a.n, wpc);
+  switch (a.NT) {
+    case 1: return launch_t<1, M>(a, wpc, smem, s);
+    case 2: return launch_t<2, M>(a, wpc, smem, s);
+    case 3: return launch_t<3, M>(a, wpc, smem, s);
+    case 4: return launch_t<4, M>(a, wpc, smem, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bmc

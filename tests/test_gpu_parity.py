@@ -1,0 +1,212 @@
+"""GPU (libbmc.so through the C-ABI) versus the fp64 oracle on seeded inputs.
+
+Element-by-element comparison (tests/parity.py for the tolerances) at sizes
+the oracle finishes in seconds spanning several CTAs and a ragged tail, plus
+the full BASELINE configuration C3 (B = 1000, the launch bench.py times) on
+sampled instances the oracle computes one by one, and the edge cases of the
+method (no obstacles, single circle, K = 0 / 1, warm start, ellipses under
+both alpha rules, the exact x~ = y~ = 0 case, q not a multiple of 32).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import Oracle  # noqa: E402
+from synth import CONFIGS, make_init, make_problem  # noqa: E402
+from tests.helpers import oracle_params  # noqa: E402
+from tests.parity import compare  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def _solver(cfg, **kw):
+    from paper_2109_13030_b200 import solver_for
+    return solver_for(cfg, device=0, **kw)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_gpu(cfg, pr, iters=None, lambda_in=None, trace=False, solver=None, **kw):
+    s = solver or _solver(cfg, **kw)
+    iters = cfg.K if iters is None else iters
+    out = s.solve(_dev(pr["init"]), _dev(pr["obs_xy"]) if cfg.n else None,
+                  _dev(pr["obs_ab"]) if cfg.n else None, pr["bnd"], iters,
+                  lambda_in=None if lambda_in is None else _dev(lambda_in), trace=trace)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def run_oracle(cfg, pr, iters=None, lambda_in=None, trace=False, **kw):
+    o = Oracle(oracle_params(cfg, **kw), cfg.n)
+    return o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"], cfg.K if iters is None else iters,
+                   lambda_in=lambda_in, trace=trace)
+
+
+def check(cfg, pr, label, iters=None, lambda_in=None, okw=None, gkw=None, trace=False):
+    okw = okw or {}
+    gkw = gkw or {}
+    g = run_gpu(cfg, pr, iters, lambda_in, trace=trace, **gkw)
+    r = run_oracle(cfg, pr, iters, lambda_in, trace=trace, **okw)
+    st = compare(cfg, g, r, cfg.res_tol, label)
+    print(st)
+    return g, r
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c1_full(seed):
+    cfg = CONFIGS["C1"]
+    check(cfg, make_problem(cfg, seed), f"C1 seed {seed}")
+
+
+def test_c2_ragged():
+    cfg = CONFIGS["C2"]
+    check(cfg, make_problem(cfg, 0, B=37), "C2 B=37")
+
+
+def test_c3_scene_small_batch():
+    cfg = CONFIGS["C3"]
+    check(cfg, make_problem(cfg, 1, B=21), "C3 B=21")
+
+
+def test_c4_tight_bounds_200_iters():
+    cfg = CONFIGS["C4"]
+    g, r = check(cfg, make_problem(cfg, 2, B=10), "C4 B=10")
+    assert np.any(r["residual"][:, 0] > 0)
+
+
+def test_c3_full_batch_sampled_instances():
+    """The bench launch (C3: B = 1000, K = 100): 16 sampled instances vs the oracle."""
+    cfg = CONFIGS["C3"]
+    pr = make_problem(cfg, 0)
+    g = run_gpu(cfg, pr)
+    idx = np.random.default_rng(123).choice(cfg.B, 16, replace=False)
+    idx[0] = 0
+    idx[-1] = cfg.B - 1
+    sub = dict(pr)
+    sub["init"] = pr["init"][idx]
+    r = run_oracle(cfg, sub)
+    gs = {k: g[k][idx] for k in ("coeffs", "cost", "residual")}
+    compare(cfg, gs, r, cfg.res_tol, "C3 B=1000 sampled", check_best=False)
+    # the GPU best must be the argmin key over all instances of its own outputs
+    feas = g["residual"][:, 0] <= cfg.res_tol
+    assert np.all(np.isfinite(g["cost"]))
+    bi = int(g["best"][0])
+    if feas.any():
+        assert feas[bi] and g["cost"][bi] == g["cost"][feas].min()
+
+
+def test_obstacle_free():
+    cfg = CONFIGS["C1"].with_(n=0, B=6)
+    check(cfg, make_problem(cfg, 0), "n=0")
+
+
+def test_single_circle_zero_offset():
+    cfg = CONFIGS["C1"].with_(m=1, B=9)
+    check(cfg, make_problem(cfg, 3), "m=1 r=0", okw=dict(r=[0.0]), gkw=dict(r=[0.0]))
+
+
+@pytest.mark.parametrize("K", [0, 1, 2])
+def test_few_iterations(K):
+    cfg = CONFIGS["C2"].with_(B=7)
+    check(cfg, make_problem(cfg, 4), f"K={K}", iters=K)
+
+
+def test_warm_start_lambda():
+    cfg = CONFIGS["C2"].with_(B=12, K=20)
+    pr = make_problem(cfg, 5)
+    first = run_oracle(cfg, pr, iters=10)
+    lam = first["lambda_out"].astype(np.float32)
+    g, r = check(cfg, pr, "warm lambda", lambda_in=lam)
+    assert np.max(np.abs(g["lambda_out"] - r["lambda_out"])) <= 1e-3 * max(1.0, np.abs(r["lambda_out"]).max())
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_ellipse_obstacles(rule):
+    cfg = CONFIGS["C2"].with_(B=9, K=60, n=6)
+    ab = np.stack([np.linspace(0.5, 1.1, 6), np.linspace(0.9, 0.4, 6)], 1)
+    pr = make_problem(cfg, 6)
+    pr["obs_ab"] = ab.astype(np.float32)
+    check(cfg, pr, f"ellipse rule {rule}", okw=dict(alpha_rule=rule), gkw=dict(alpha_rule=rule))
+
+
+def test_exact_zero_offset_G18():
+    """Circle centre exactly on an obstacle centre (x~ = y~ = 0): alpha := 0 (G18)."""
+    cfg = CONFIGS["C1"].with_(m=1, n=2, B=4, K=5)
+    pr = make_problem(cfg, 0)
+    pr["obs_xy"][0, :, :] = 0.0        # static obstacle sitting on the start point (0, 0)
+    check(cfg, pr, "G18", okw=dict(r=[0.0]), gkw=dict(r=[0.0]))
+
+
+@pytest.mark.parametrize("q", [32, 64, 77, 128])
+def test_horizon_sizes(q):
+    cfg = CONFIGS["C2"].with_(q=q, B=5, K=30)
+    check(cfg, make_problem(cfg, 7), f"q={q}")
+
+
+@pytest.mark.parametrize("m", [4, 8])
+def test_many_circles(m):
+    cfg = CONFIGS["C2"].with_(m=m, B=5, K=30)
+    check(cfg, make_problem(cfg, 8), f"m={m}")
+
+
+def test_res_trace():
+    cfg = CONFIGS["C1"].with_(B=5)
+    pr = make_problem(cfg, 0)
+    g = run_gpu(cfg, pr, trace=True)
+    r = run_oracle(cfg, pr, trace=True)
+    tol = 1e-4 * np.abs(r["res_trace"]) + 2e-5
+    assert np.all(np.abs(g["res_trace"] - r["res_trace"]) <= tol)
+    assert np.allclose(g["res_trace"][:, -1], g["residual"][:, 0])
+
+
+def test_determinism_and_batch_independence():
+    cfg = CONFIGS["C3"].with_(B=64, K=30)
+    pr = make_problem(cfg, 0)
+    s = _solver(cfg)
+    a = run_gpu(cfg, pr, solver=s)
+    b = run_gpu(cfg, pr, solver=s)
+    for k in ("coeffs", "lambda_out", "residual", "cost", "best"):
+        assert np.array_equal(a[k], b[k]), k
+    sub = dict(pr)
+    sub["init"] = pr["init"][17:29]
+    c = run_gpu(cfg, sub, solver=s)
+    assert np.array_equal(c["coeffs"], a["coeffs"][17:29])
+    assert np.array_equal(c["residual"], a["residual"][17:29])
+
+
+def test_index_base_and_host_path():
+    cfg = CONFIGS["C2"].with_(B=10, K=15)
+    pr = make_problem(cfg, 9)
+    s = _solver(cfg)
+    out = s.solve(_dev(pr["init"]), _dev(pr["obs_xy"]), _dev(pr["obs_ab"]), pr["bnd"], cfg.K, index_base=1000)
+    torch.cuda.synchronize()
+    best = out["best"].cpu().numpy()
+    assert 1000 <= best[0] < 1010 and (best[1] & ((1 << 30) - 1)) == best[0]
+    h = s.solve_host(pr["init"], pr["obs_xy"], pr["obs_ab"], pr["bnd"], cfg.K, index_base=1000)
+    assert np.array_equal(h["coeffs"], out["coeffs"].cpu().numpy())
+    assert np.array_equal(h["best"], best)
+
+
+def test_error_codes():
+    from paper_2109_13030_b200 import BmcError
+    cfg = CONFIGS["C1"]
+    pr = make_problem(cfg, 0)
+    s = _solver(cfg)
+    with pytest.raises(BmcError) as e:
+        s.solve(_dev(pr["init"]), _dev(pr["obs_xy"]), _dev(pr["obs_ab"]), pr["bnd"], -1)
+    assert e.value.code == 1
+    big = np.zeros((161, 2, cfg.q), np.float32)
+    with pytest.raises(BmcError):
+        s.solve(_dev(pr["init"]), _dev(big), _dev(np.ones((161, 2), np.float32)), pr["bnd"], 3)
