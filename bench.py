@@ -1,0 +1,314 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched AM iteration (arXiv 2109.13030) on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A step is one whole batch solve: BASELINE configuration C3 per GPU (batch 1000,
+horizon 100, 3 circles, 30 dynamic obstacles, 100 AM iterations, seeded
+synthetic scene), i.e. every row of the hot path (xi1, xi2, xi3, xi4, lambda,
+residual, cost, argmin) plus, for N > 1, the best-of-batch exchange over NCCL.
+Weak scaling: every rank solves its own 1000-instance shard of an N*1000 batch.
+
+`value` = trajectories*iterations per second over all ranks, from CUDA events
+around each step on the launching stream (max over ranks); L2 is flushed
+(256 MiB memset) between steps, outside the events.  `e2e` measures the same
+through the host-buffer C-ABI call (bmc_solve_host: pinned H2D of the inputs,
+kernel, D2H of every output, synchronise).  `roofline` reports the fused
+kernel against the FP32 issue peak; `cpu_baseline` is
+the fp64 oracle timed on a bounded sample on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, make_problem  # noqa: E402
+
+
+def algorithmic_fp32_ops(q: int, m: int, n: int) -> float:
+    """FP32 lane-instructions per (instance, iteration) of the method as formulated
+    (DESIGN.md "Roofline"): per sample t, evaluation of x, y, psi, c, s and the
+    first/second derivatives (9 x 11 FMA), the F^T(F xi - g) and P^T theta
+    contractions (9 x 11 FMA), the velocity/acceleration projections and
+    per-sample bookkeeping (20 + 6 m), and per (circle, obstacle) the
+    branch-free closed-form projection with its two accumulations (8)."""
+    return float(q) * (99 + 99 + 20 + 6 * m + 8 * m * n)
+
+
+def fp32_peak(sm_mhz: float, sms: int = 148) -> float:
+    return sms * 128 * sm_mhz * 1e6   # lane-instructions per second
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", ",".join(str(g) for g in self.gpus),
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg, pr, sample: int, iters: int):
+    """The fp64 oracle, as it stands, on this host's cores (bounded sample)."""
+    from oracle import Oracle, OracleParams
+    o = Oracle(OracleParams(q=cfg.q, T=cfg.T, degree=cfg.degree, r=cfg.offsets, v_max=cfg.v_max,
+                            a_max=cfg.a_max, rho=cfg.rho, rho_psi=cfg.rho_psi, res_tol=cfg.res_tol), cfg.n)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"][:sample], iters, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return dict(value=sample * iters / dt, unit="trajectories*iterations/s", cores=cores, kind="oracle",
+                sample=f"{sample} instances x {iters} iterations of the {cfg.name} scene "
+                       f"(fp64 C oracle, OpenMP over instances), {dt:.2f} s wall")
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    if rank != 0:
+        return
+    pr = make_problem(cfg, 0)
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, pr, max(1, sample // 4), cfg.K)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cb = cpu_baseline(cfg, pr, sample, cfg.K)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = args.steps * sample * cfg.K / tot
+    line = dict(impl="reference", metric=METRIC, value=value, unit="trajectories*iterations/s",
+                n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=1e3 * tot / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64", data="synthetic",
+                config=workload(cfg, world) | {"reference_sample_instances": sample},
+                cpu_baseline=dict(kind="oracle", cores=cb["cores"], sample=cb["sample"], value=value,
+                                  unit="trajectories*iterations/s"),
+                e2e=dict(value=value, unit="trajectories*iterations/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "trajectories*iterations/s (batch solve: 1000 instances/GPU x 100 AM iterations)"
+
+
+def workload(cfg, world):
+    return {"workload": f"{cfg.name}: batch {cfg.B}/GPU, horizon {cfg.q}, {cfg.m} circles, {cfg.n} "
+                        f"{'dynamic' if cfg.dynamic else 'static'} obstacles, {cfg.K} AM iterations",
+            "batch_per_gpu": cfg.B, "global_batch": cfg.B * world, "q": cfg.q, "m": cfg.m, "n_obs": cfg.n,
+            "iters": cfg.K, "l2": "flushed between steps (256 MiB memset, outside the timed events)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--batch", type=int, default=None, help="override instances per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=16)
+    ap.add_argument("--cpu-sample", type=int, default=48)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.batch:
+        cfg = cfg.with_(B=args.batch)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    from paper_2109_13030_b200 import solver_for
+    from paper_2109_13030_b200.distributed import BestExchange
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    # every rank builds the same scene from the seed; rank r owns instances [r B, (r+1) B)
+    glob = make_problem(cfg, 0, B=cfg.B * world)
+    shard = slice(rank * cfg.B, (rank + 1) * cfg.B)
+    init_h = np.ascontiguousarray(glob["init"][shard])
+    init = torch.from_numpy(init_h).to(dev)
+    obs = torch.from_numpy(glob["obs_xy"]).to(dev)
+    ab = torch.from_numpy(glob["obs_ab"]).to(dev)
+    solver = solver_for(cfg, device=local)
+    xchg = BestExchange(pg, dev) if world > 1 else None
+    out = solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out)
+        if xchg is not None:
+            xchg.exchange(out["best"], out["coeffs"], rank * cfg.B)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    if pg is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler([local]) as clk:
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            kev[i][0].record(stream)
+            solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out)
+            launches += solver.last_launches
+            kev[i][1].record(stream)
+            if xchg is not None:
+                xchg.exchange(out["best"], out["coeffs"], rank * cfg.B)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if pg is not None:
+            torch.distributed.barrier()
+        wall = time.perf_counter() - wall0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    t_dev = sum(step_ms) / 1e3
+    if pg is not None:
+        tt = torch.tensor([t_dev, sum(kern_ms) / 1e3], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_dev, t_kern = float(tt[0]), float(tt[1])
+    else:
+        t_kern = sum(kern_ms) / 1e3
+    value = world * cfg.B * cfg.K * args.steps / t_dev
+
+    # ---- end to end through the host-buffer C-ABI (bmc_solve_host) ------------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    h_init, h_obs, h_ab = pin(init_h), pin(glob["obs_xy"]), pin(glob["obs_ab"])
+    B = cfg.B
+    h_out = dict(coeffs=pin(np.empty((B, 5, 11), np.float32)), lambda_out=pin(np.empty((B, 5, 11), np.float32)),
+                 residual=pin(np.empty((B, 2), np.float32)), cost=pin(np.empty((B,), np.float32)),
+                 best=pin(np.empty((2,), np.int64)))
+    for _ in range(args.warmup):
+        solver.solve_host(h_init, h_obs, h_ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=h_out)
+    e2e_t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        solver.solve_host(h_init, h_obs, h_ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=h_out)
+        e2e_t.append(time.perf_counter() - t0)
+    t_e2e = sum(e2e_t)
+    if pg is not None:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    e2e_value = world * cfg.B * cfg.K * args.steps / t_e2e
+    h2d = h_init.nbytes + h_obs.nbytes + h_ab.nbytes
+    d2h = sum(v.nbytes for v in h_out.values())
+
+    if rank != 0:
+        if pg is not None:
+            torch.distributed.destroy_process_group()
+        return
+    clocks = clk.summary()
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    ops = algorithmic_fp32_ops(cfg.q, cfg.m, cfg.n) * cfg.B * cfg.K      # per launch
+    kern_avg = t_kern / args.steps
+    achieved = ops / kern_avg
+    peak = fp32_peak(sm_max)
+    roof = dict(bound="alu", achieved=achieved / 1e12, peak=peak / 1e12,
+                unit="T FP32 lane-instr/s", frac=achieved / peak, traffic=None,
+                kernel="bmc_am_kernel<3>", algorithmic_ops_per_launch=ops,
+                kernel_ms=1e3 * kern_avg,
+                peak_basis=f"148 SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)")
+    if clocks.get("sm_mhz"):
+        roof["frac_at_observed_clock"] = achieved / fp32_peak(clocks["sm_mhz"])
+    traffic_file = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            roof["traffic"] = json.load(open(traffic_file)).get(f"{cfg.name}_bytes_per_launch")
+        except Exception:
+            pass
+    line = dict(metric=METRIC, value=value, unit="trajectories*iterations/s", n_gpus=world, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * t_dev / args.steps, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f32 (fp64 KKT steps)", data="synthetic",
+                config=workload(cfg, world), clocks=clocks, gpu_launches=launches,
+                e2e=dict(value=e2e_value, unit="trajectories*iterations/s", h2d_bytes_per_step=int(h2d),
+                         d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * t_e2e / args.steps),
+                roofline=roof, wall_s=wall)
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, glob, args.cpu_sample, cfg.K)
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,24 @@ int32_t bmc_solve(bmc_ctx* ctx, const bmc_problem* prob, const bmc_result* res,
  * and errors as bmc_solve. */
 int32_t bmc_solve_host(bmc_ctx* ctx, const bmc_problem* prob_host, const bmc_result* res_host);
 
+/* ---- multi-GPU best-of-batch exchange ----------------------
+ * A batch sharded over ranks (bmc_problem.index_base = first global index of
+ * the shard) has one global argmin: the minimum packed key over all ranks.
+ * Record layout (BMC_RECORD_WORDS int64 per rank, device memory):
+ *   word 0 = packed key, words 1.. = the 55 fp32 coefficients of that
+ *   instance (c_x, c_c, c_y, c_s, c_psi), zero padded.
+ * bmc_pack_best writes this rank's record from the `best` and `coeffs` of a
+ * finished bmc_solve (stream-ordered after it); the caller all-gathers the
+ * records (e.g. NCCL all_gather over NVLink); bmc_select_best picks the
+ * minimum key and writes best_out[2] = {global index, key} and
+ * coeffs_out[55].  Both are one-warp kernels on `stream`.  Errors:
+ * BMC_EINVAL (NULL pointer, nranks < 1), BMC_ECUDA (launch failure). */
+#define BMC_RECORD_WORDS 32
+int32_t bmc_pack_best(const int64_t* best, const float* coeffs, int64_t index_base, int64_t* record,
+                      bmc_stream_t stream);
+int32_t bmc_select_best(const int64_t* records, int32_t nranks, int64_t* best_out, float* coeffs_out,
+                        bmc_stream_t stream);
+
 /* Kernel launches issued by the last bmc_solve / bmc_solve_host on ctx. */
 int32_t bmc_last_launch_count(const bmc_ctx* ctx);
 

@@ -71,6 +71,10 @@ def load_library(path: str = LIBPATH):
         L.bmc_version.restype = C.c_int32
         L.bmc_last_launch_count.argtypes = [C.c_void_p]
         L.bmc_last_launch_count.restype = C.c_int32
+        L.bmc_pack_best.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.bmc_pack_best.restype = C.c_int32
+        L.bmc_select_best.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.bmc_select_best.restype = C.c_int32
         _lib = L
     return _lib
 

@@ -284,6 +284,14 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
     for (int ch = 0; ch < 3; ++ch) a.b[ch][r] = pr->bnd[ch][bit];
     ++r;
   }
+  a.T = c->p.T;
+  // reference line for the fp32 deviation frame: start -> goal position when
+  // both are constrained, else the start (or the origin)
+  const bool has0 = c->p.boundary_mask & 1u, hasT = c->p.boundary_mask & 8u;
+  a.ref_x0 = has0 ? pr->bnd[0][0] : (hasT ? pr->bnd[0][3] : 0.0);
+  a.ref_y0 = has0 ? pr->bnd[1][0] : (hasT ? pr->bnd[1][3] : 0.0);
+  a.ref_dx = (has0 && hasT) ? pr->bnd[0][3] - pr->bnd[0][0] : 0.0;
+  a.ref_dy = (has0 && hasT) ? pr->bnd[1][3] - pr->bnd[1][0] : 0.0;
   cudaError_t e = launch_am(a, wpc, s);
   c->last_launches = 1;
   if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");

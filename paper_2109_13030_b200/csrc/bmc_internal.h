@@ -62,8 +62,11 @@ struct KernelArgs {
   float r[M_MAX];
   float nR1, nR2p1;            // n sum r_i, n sum r_i^2 + 1 (F^T F closed form)
   float v_max, a_max;
-  double rho, rho_psi, res_tol;
+  double rho, rho_psi, res_tol, T;
   double b[3][NB_MAX];         // selected boundary values: x, y, psi
+  // boundary line x_ref(t) = ref_x0 + ref_dx t/T (same for y): positions are
+  // evaluated in fp32 as deviations from it
+  double ref_x0, ref_dx, ref_y0, ref_dy;
 };
 
 struct SetupParams {

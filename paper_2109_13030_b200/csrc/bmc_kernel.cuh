@@ -3,32 +3,38 @@
 // One warp owns one batch instance l for all K iterations (instances are
 // independent, "each instance in the batch is independent"); a CTA of
 // WPC warps shares one shared-memory copy of the batch-invariant data: the
-// basis P, Pdot, Pddot, the KKT inverses (bulk-copied by TMA, cp.async.bulk)
-// and the obstacle trajectories.  Lanes own time samples t = lane + 32 u.
+// basis P, Pdot, Pddot and the KKT inverses (bulk-copied by TMA,
+// cp.async.bulk + mbarrier) and the obstacle trajectories.
+//
+// Time samples are processed in rounds of 32 lanes (t = 32 u + lane).  The
+// last, partial round (q mod 32 samples) splits the obstacles over lane
+// groups instead of idling lanes: R = next_pow2(q mod 32) lanes per group,
+// S = 32 / R groups, group g takes obstacles j = g, g + S, ..., and the
+// per-sample sums are combined by xor-shuffles across groups.
 //
 // Per iteration (paper step order):
 //   A  xi1 step (Eq. 13/17 via Eq. 4):  xi1' = M xi1 + K11 (lambda - rho h) + K12 b
-//      in fp64 (lanes k < 22 own row k of both channels);
+//      in fp64 (lane k < 22 owns row k of both channels);
 //   B  c, s = P c_c, P c_s; theta = atan2(s, c); P^T theta (warp transpose-reduce);
 //   C  xi2 step (Eq. 19) and lambda_psi (Eq. 23b, G4) in fp64 (lanes k < 11);
-//   D  x, xdot, xddot, y, ..., psi at the lane's t; velocity / acceleration
-//      projections (Eq. 21b-c, 22b-c: projection onto the v_max / a_max disk);
-//      collision projections over all (j, i) (Eq. 21a, 22a) reduced in
-//      registers to D = sum_ij delta_ij and E = sum_i r_i sum_j delta_ij,
-//      delta_ij = (a d cos(alpha), b d sin(alpha)) - (x~, y~), then the
-//      contraction h = F^T (F xi1 - g) (Eq. 10-11 closed form):
+//   D  x, xdot, xddot, y, ..., psi at the lane's t (deviation from the boundary
+//      line, fp32); velocity / acceleration projections (Eq. 21b-c, 22b-c:
+//      projection onto the v_max / a_max disk); collision projections over all
+//      (j, i) (Eq. 21a, 22a) reduced in registers to D = sum_ij delta_ij and
+//      E = sum_i r_i sum_j delta_ij, delta_ij = (a d cos alpha, b d sin alpha)
+//      - (x~, y~); then the contraction h = F^T (F xi1 - g) in closed form
+//      (Eq. 10-11):
 //        h_pos  = P^T (n R1 e - D) - Pd^T dv - Pdd^T da,
 //        h_copy = P^T ((n R2 + 1) e - E),      e = c - cos(psi)  (G9)
 //   E  lambda <- lambda - rho h (Eq. 23a with F^T, G3).
 // The residual r1 = ||F xi1 - g|| is accumulated in the last iteration (or
 // every iteration in trace mode) from the same per-row quantities.
+#pragma once
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include "bmc_internal.h"
-
-#pragma once
 
 namespace bmc {
 
@@ -41,9 +47,10 @@ struct WarpSmem {
   double rhs[2 * NV2];  // [k][ch]
   double xi2[12];
   double rhsp[12];
-  float cf[5][12];      // fp32 copies of c_x, c_c, c_y, c_s, c_psi (padded)
+  float cf[5][12];      // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s, c_psi (padded)
   float h[48];
   float pth[16];
+  float c[Q_MAX], s[Q_MAX], th[Q_MAX];   // copies c, s and theta per sample
 };
 static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
 
@@ -83,6 +90,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
         : "r"(smem_u32(bar)), "r"(phase)
         : "memory");
   }
+}
+// MUFU.RSQ without the denormal fix-up sequence (x = 0 -> +inf).
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // ------------------------------------------------------------ warp reductions
@@ -134,43 +147,76 @@ __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
   c[8] = d.x; c[9] = d.y; c[10] = d.z;
 }
 
+// Round u of the sample loop: sample t, obstacle group g of S groups, R lanes per group.
+struct Round {
+  int t, g, S, R;
+};
+__device__ __forceinline__ Round make_round(int u, int ntf, int rtail, int lane) {
+  Round r;
+  if (u < ntf) {
+    r.t = 32 * u + lane; r.g = 0; r.S = 1; r.R = 32;
+  } else {
+    r.R = rtail; r.S = 32 / rtail;
+    r.t = 32 * ntf + (lane & (rtail - 1)); r.g = lane / rtail;
+  }
+  return r;
+}
+
 // --------------------------------------------------- collision projections
-// For every obstacle j and circle i at the lane's t: x~ = X_i - x_j,
-// y~ = Y_i - y_j (X_i = x + r_i cos psi, G9), and the closed-form offset
-// delta = (a d cos(alpha), b d sin(alpha)) - (x~, y~) of Eq. 21a/22a:
+// For every obstacle j of the lane's group and circle i at sample t:
+// x~ = X_i - x_j, y~ = Y_i - y_j (X_i = x + r_i cos psi, G9) and the
+// closed-form offset delta = (a d cos alpha, b d sin alpha) - (x~, y~) of
+// Eq. 21a / 22a:
 //   kind 0 (a == b, either rule):  delta = (x~, y~) max(a / |(x~,y~)| - 1, 0)
 //   kind 1 (literal atan2(y~,x~)): delta = (x~ (a f - 1), y~ (b f - 1)),
 //                                  f = max(1/rho, (a x~^2 + b y~^2)/(a^2 x~^2 + b^2 y~^2))
 //   kind 2 (scaled, G8):           delta = (x~, y~) max(ab / sqrt(b^2 x~^2 + a^2 y~^2) - 1, 0)
+// For kind 0, delta = 0 unless |(x~,y~)| < a: the rsqrt path runs only when
+// some lane of the warp is inside (warp-uniform branch).  The residual terms
+// (r_i e - delta)^2 are accumulated as base + delta (delta - 2 r_i e).
 // GUARD handles x~ = y~ = 0 exactly (G18: alpha = 0, d = 1 -> delta = (a, 0)).
-template <int M, bool RES, bool GUARD>
+// SPLIT (tail round): lanes of different groups visit different obstacles, so
+// the trip count is made uniform with far-away dummy obstacles and the vote
+// runs over the active mask.
+template <int M, bool RES, bool GUARD, bool SPLIT>
 __device__ __forceinline__ void coll_loop(const float2* __restrict__ ob, const float4* __restrict__ abi,
-                                          int n, int QP, const float (&X)[M], const float (&Y)[M],
-                                          const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
-                                          float (&Dy)[M], float& rc) {
+                                          int n, int QP, int g, int S, const float (&X)[M],
+                                          const float (&Y)[M], const float (&rec)[M], const float (&res_s)[M],
+                                          float (&Dx)[M], float (&Dy)[M], float& rc) {
+  const int trips = SPLIT ? (n + S - 1) / S : n;
 #pragma unroll 2
-  for (int j = 0; j < n; ++j) {
-    const float2 o = ob[(size_t)j * QP];
-    const float4 ab = abi[j];
+  for (int it = 0; it < trips; ++it) {
+    float2 o;
+    float4 ab;
+    if (SPLIT) {
+      const int j = g + it * S;
+      const bool have = j < n;
+      o = ob[(size_t)(have ? j : 0) * QP];
+      ab = abi[have ? j : 0];
+      if (!have) { o = make_float2(1.0e4f, 1.0e4f); ab = make_float4(1.f, 1.f, 1.f, 0.f); }
+    } else {
+      o = ob[(size_t)it * QP];
+      ab = abi[it];
+    }
     if (ab.w == 0.f) {
+      float xt[M], yt[M], r2[M];
+      float rmin = 3.0e38f;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
-        const float xt = X[i] - o.x, yt = Y[i] - o.y;
-        const float r2 = fmaf(yt, yt, xt * xt);
-        const float sc = fmaxf(fmaf(ab.x, rsqrtf(r2), -1.f), 0.f);
-        if (!RES && !GUARD) {
-          Dx[i] = fmaf(sc, xt, Dx[i]);
-          Dy[i] = fmaf(sc, yt, Dy[i]);
-        } else {
-          float dx = sc * xt, dy = sc * yt;
-          if (GUARD && r2 == 0.f) { dx = ab.x; dy = 0.f; }
+        xt[i] = X[i] - o.x;
+        yt[i] = Y[i] - o.y;
+        r2[i] = fmaf(yt[i], yt[i], xt[i] * xt[i]);
+        rmin = fminf(rmin, r2[i]);
+      }
+      if (__any_sync(SPLIT ? __activemask() : FULL, rmin < ab.z)) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          const float sc = fmaxf(fmaf(ab.x, rsqrt_ftz(r2[i]), -1.f), 0.f);
+          float dx = sc * xt[i], dy = sc * yt[i];
+          if (GUARD && r2[i] == 0.f) { dx = ab.x; dy = 0.f; }
           Dx[i] += dx;
           Dy[i] += dy;
-          if (RES) {
-            const float tx = rec[i] - dx, ty = res_s[i] - dy;
-            rc = fmaf(tx, tx, rc);
-            rc = fmaf(ty, ty, rc);
-          }
+          if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
         }
       }
     } else {
@@ -182,43 +228,45 @@ __device__ __forceinline__ void coll_loop(const float2* __restrict__ ob, const f
         float dx, dy;
         if (ab.w == 1.f) {
           const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
-          const float f = fmaxf(rsqrtf(x2 + y2), __fdividef(N, D));
+          const float f = fmaxf(rsqrt_ftz(x2 + y2), __fdividef(N, D));
           dx = xt * fmaf(a, f, -1.f);
           dy = yt * fmaf(b, f, -1.f);
         } else {
           const float R2 = fmaf(a * a, y2, b * b * x2);
-          const float sc = fmaxf(fmaf(ab.z, rsqrtf(R2), -1.f), 0.f);
+          const float sc = fmaxf(fmaf(ab.z, rsqrt_ftz(R2), -1.f), 0.f);
           dx = sc * xt;
           dy = sc * yt;
         }
         if (GUARD && x2 + y2 == 0.f) { dx = a; dy = 0.f; }
         Dx[i] += dx;
         Dy[i] += dy;
-        if (RES) {
-          const float tx = rec[i] - dx, ty = res_s[i] - dy;
-          rc = fmaf(tx, tx, rc);
-          rc = fmaf(ty, ty, rc);
-        }
+        if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
       }
     }
   }
 }
 
+template <int M, bool RES>
+__device__ __noinline__ void coll_loop_guarded(const float2* __restrict__ ob, const float4* __restrict__ abi,
+                                               int n, int QP, int g, int S, const float (&X)[M],
+                                               const float (&Y)[M], const float (&rec)[M],
+                                               const float (&res_s)[M], float (&Dx)[M], float (&Dy)[M],
+                                               float& rc) {
+  coll_loop<M, RES, true, true>(ob, abi, n, QP, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+}
+
 // ---------------------------------------------------------------- phase B
-// c, s at the lane's samples, theta = atan2(s, c) (Eq. 19; G18), and
-// the warp total of P^T theta written to ws->pth[0..10].
-template <int NT>
-__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, int QP, WarpSmem* ws, int lane,
-                                            float (&cr)[NT], float (&sr)[NT], float (&th)[NT]) {
+// c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
+// warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
+__device__ __noinline__ void phase_theta(const float* __restrict__ Pt, int QP, WarpSmem* ws, int lane) {
   float cc[NV], cs[NV];
   load12(ws->cf[1], cc);
   load12(ws->cf[3], cs);
   float acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.f;
-#pragma unroll
-  for (int u = 0; u < NT; ++u) {
-    const int t = lane + 32 * u;
+#pragma unroll 1
+  for (int t = lane; t < QP; t += 32) {
     float p[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
@@ -229,9 +277,9 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, int QP
       s = fmaf(p[k], cs[k], s);
     }
     const float tht = (c == 0.f && s == 0.f) ? 0.f : atan2f(s, c);
-    cr[u] = c;
-    sr[u] = s;
-    th[u] = tht;
+    ws->c[t] = c;
+    ws->s[t] = s;
+    ws->th[t] = tht;
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = fmaf(p[k], tht, acc[k]);
   }
@@ -239,22 +287,32 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, int QP
   if (!(lane & 1) && (lane >> 1) < NV) ws->pth[lane >> 1] = v;
 }
 
+struct ProjArgs {
+  const float* Pt;
+  const float2* obs;
+  const float4* abi;
+  int QP, q, n, ntf, rtail, rounds;
+  float r[M_MAX];
+  float nR1, nR2p1, v_max, a_max, vref_x, vref_y;
+};
+
 // ---------------------------------------------------------------- phase D
-template <int NT, int M, bool RES>
-__device__ __forceinline__ void phase_project(const KernelArgs& a, const float* __restrict__ Pt,
-                                              const float2* __restrict__ obs, const float4* __restrict__ abi,
-                                              WarpSmem* ws, int lane, const float (&cr)[NT],
-                                              const float (&sr)[NT], const float (&th)[NT], float& res_out,
-                                              float& rpsi_out) {
-  const int QP = a.QP, q = a.q, n = a.n;
+template <int M, bool RES>
+__device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int lane, float* res_out,
+                                           float* rpsi_out) {
+  const int QP = pa.QP, q = pa.q, n = pa.n;
+  const float* __restrict__ Pt = pa.Pt;
   float acc[48];
 #pragma unroll
   for (int k = 0; k < 48; ++k) acc[k] = 0.f;
   float res = 0.f, rps = 0.f;
-#pragma unroll
-  for (int u = 0; u < NT; ++u) {
-    const int t = lane + 32 * u;
-    float x = 0.f, y = 0.f, xd = 0.f, yd = 0.f, xdd = 0.f, ydd = 0.f, psi = 0.f;
+#pragma unroll 1
+  for (int u = 0; u < pa.rounds; ++u) {
+    const Round rd = make_round(u, pa.ntf, pa.rtail, lane);
+    const int t = rd.t;
+    const bool own = (rd.g == 0);               // group 0 owns the sample's contributions
+    const bool valid = own && (t < q);
+    float x = 0.f, y = 0.f, xd = pa.vref_x, yd = pa.vref_y, xdd = 0.f, ydd = 0.f, psi = 0.f;
     {
       float cx[NV], cy[NV], cp[NV];
       load12(ws->cf[0], cx);
@@ -278,31 +336,36 @@ __device__ __forceinline__ void phase_project(const KernelArgs& a, const float* 
         ydd = fmaf(pdd[k], cy[k], ydd);
       }
       // velocity / acceleration: g = projection onto the bound disk (G6, G7)
-      const float sv = fminf(fmaf(a.v_max, rsqrtf(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
-      const float sa = fminf(fmaf(a.a_max, rsqrtf(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
+      const float sv = fminf(fmaf(pa.v_max, rsqrt_ftz(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
+      const float sa = fminf(fmaf(pa.a_max, rsqrt_ftz(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
+      const float w = own ? -1.f : 0.f;
       const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        acc[k] = fmaf(pd[k], -dvx, fmaf(pdd[k], -dax, acc[k]));
-        acc[NV2 + k] = fmaf(pd[k], -dvy, fmaf(pdd[k], -day, acc[NV2 + k]));
+        acc[k] = fmaf(pd[k], w * dvx, fmaf(pdd[k], w * dax, acc[k]));
+        acc[NV2 + k] = fmaf(pd[k], w * dvy, fmaf(pdd[k], w * day, acc[NV2 + k]));
       }
-      if (RES && t < q) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
+      if (RES && valid) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
     }
     float sp, cps;
     sincosf(psi, &sp, &cps);
-    const float ec = cr[u] - cps, es = sr[u] - sp;
+    const float ec = ws->c[t] - cps, es = ws->s[t] - sp;
     float X[M], Y[M], Dx[M], Dy[M], rec[M], res_s[M];
+    float base = 0.f;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      X[i] = fmaf(a.r[i], cps, x);
-      Y[i] = fmaf(a.r[i], sp, y);
+      X[i] = fmaf(pa.r[i], cps, x);
+      Y[i] = fmaf(pa.r[i], sp, y);
       Dx[i] = 0.f;
       Dy[i] = 0.f;
-      rec[i] = a.r[i] * ec;
-      res_s[i] = a.r[i] * es;
+      rec[i] = pa.r[i] * ec;
+      res_s[i] = pa.r[i] * es;
+      base = fmaf(rec[i], rec[i], fmaf(res_s[i], res_s[i], base));
     }
     float rc = 0.f;
-    coll_loop<M, RES, false>(obs + t, abi, n, QP, X, Y, rec, res_s, Dx, Dy, rc);
+    const float2* ob = pa.obs + t;
+    if (rd.S == 1) coll_loop<M, RES, false, false>(ob, pa.abi, n, QP, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
+    else coll_loop<M, RES, false, true>(ob, pa.abi, n, QP, rd.g, rd.S, X, Y, rec, res_s, Dx, Dy, rc);
     float chk = rc;
 #pragma unroll
     for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
@@ -310,18 +373,27 @@ __device__ __forceinline__ void phase_project(const KernelArgs& a, const float* 
 #pragma unroll
       for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
       rc = 0.f;
-      coll_loop<M, RES, true>(obs + t, abi, n, QP, X, Y, rec, res_s, Dx, Dy, rc);
+      coll_loop_guarded<M, RES>(ob, pa.abi, n, QP, rd.g, rd.S, X, Y, rec, res_s, Dx, Dy, rc);
+    }
+    for (int off = rd.R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        Dx[i] += __shfl_xor_sync(FULL, Dx[i], off);
+        Dy[i] += __shfl_xor_sync(FULL, Dy[i], off);
+      }
+      if (RES) rc += __shfl_xor_sync(FULL, rc, off);
     }
     float Ds_x = 0.f, Ds_y = 0.f, Ex = 0.f, Ey = 0.f;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       Ds_x += Dx[i];
       Ds_y += Dy[i];
-      Ex = fmaf(a.r[i], Dx[i], Ex);
-      Ey = fmaf(a.r[i], Dy[i], Ey);
+      Ex = fmaf(pa.r[i], Dx[i], Ex);
+      Ey = fmaf(pa.r[i], Dy[i], Ey);
     }
-    const float u1x = fmaf(a.nR1, ec, -Ds_x), u1y = fmaf(a.nR1, es, -Ds_y);
-    const float vx = fmaf(a.nR2p1, ec, -Ex), vy = fmaf(a.nR2p1, es, -Ey);
+    const float w = own ? 1.f : 0.f;
+    const float u1x = w * fmaf(pa.nR1, ec, -Ds_x), u1y = w * fmaf(pa.nR1, es, -Ds_y);
+    const float vx = w * fmaf(pa.nR2p1, ec, -Ex), vy = w * fmaf(pa.nR2p1, es, -Ey);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const float p = Pt[k * QP + t];
@@ -330,9 +402,10 @@ __device__ __forceinline__ void phase_project(const KernelArgs& a, const float* 
       acc[NV2 + k] = fmaf(p, u1y, acc[NV2 + k]);
       acc[NV2 + NV + k] = fmaf(p, vy, acc[NV2 + NV + k]);
     }
-    if (t < q) {
-      if (RES) res += rc + ec * ec + es * es;
-      rps = fmaf(th[u] - psi, th[u] - psi, rps);
+    if (valid) {
+      if (RES) res += fmaf((float)n, base, rc) + ec * ec + es * es;
+      const float dth = ws->th[t] - psi;
+      rps = fmaf(dth, dth, rps);
     }
   }
   const float v32 = transpose_reduce32(acc, lane);
@@ -340,14 +413,14 @@ __device__ __forceinline__ void phase_project(const KernelArgs& a, const float* 
   ws->h[lane] = v32;
   if (!(lane & 1)) ws->h[32 + (lane >> 1)] = v16;
   if (RES) {
-    res_out = warp_sum(res);
-    rpsi_out = warp_sum(rps);
+    *res_out = warp_sum(res);
+    *rpsi_out = warp_sum(rps);
   }
 }
 
 // ---------------------------------------------------------------- kernel
-template <int NT, int M>
-__global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
+template <int M>
+__global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
   const int QP = a.QP, n = a.n, q = a.q, K = a.iters;
@@ -372,16 +445,23 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
       bulk_g2s(smem + off, a.blob + off, nbytes, mbar);
     }
   }
+  // obstacles relative to the boundary line (x_ref(t), y_ref(t)), computed in
+  // fp64 and rounded once; padding samples far away
+  const double inv_q1 = 1.0 / (double)(q - 1);
   for (int idx = tid; idx < n * QP; idx += blockDim.x) {
     const int j = idx / QP, t = idx - j * QP;
-    float2 v = make_float2(1.0e4f, 1.0e4f);   // padding samples: far away, delta = 0
-    if (t < q) v = make_float2(__ldg(a.obs_xy + (size_t)(2 * j) * q + t), __ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t));
+    float2 v = make_float2(1.0e4f, 1.0e4f);
+    if (t < q) {
+      const double tau = (double)t * inv_q1;
+      v = make_float2((float)((double)__ldg(a.obs_xy + (size_t)(2 * j) * q + t) - fma(a.ref_dx, tau, a.ref_x0)),
+                      (float)((double)__ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t) - fma(a.ref_dy, tau, a.ref_y0)));
+    }
     obs[idx] = v;
   }
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
-    abi[j] = make_float4(aa, bb, aa * bb, kind);
+    abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
   }
   for (int i = tid; i < wpc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
   mbar_wait(mbar, 0);
@@ -402,10 +482,37 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
   }
   __syncthreads();
 
+  ProjArgs pa;
+  pa.Pt = Pt;
+  pa.obs = obs;
+  pa.abi = abi;
+  pa.QP = QP;
+  pa.q = q;
+  pa.n = n;
+  pa.ntf = q / 32;
+  {
+    const int rem = q - 32 * pa.ntf;
+    int R = 1;
+    while (R < rem) R <<= 1;
+    pa.rtail = R;
+    pa.rounds = pa.ntf + (rem > 0 ? 1 : 0);
+  }
+#pragma unroll
+  for (int i = 0; i < M_MAX; ++i) pa.r[i] = a.r[i];
+  pa.nR1 = a.nR1;
+  pa.nR2p1 = a.nR2p1;
+  pa.v_max = a.v_max;
+  pa.a_max = a.a_max;
+  pa.vref_x = (float)(a.ref_dx / a.T);
+  pa.vref_y = (float)(a.ref_dy / a.T);
+
   const long long l = (long long)blockIdx.x * wpc + warp;
   if (l < a.B) {
     const int k = lane;
     const double rho = a.rho, rho_psi = a.rho_psi;
+    // Bernstein control points of the boundary line (linear precision: c_k = x0 + dx k / 10)
+    const double crefx = (k < NV) ? fma(a.ref_dx, (double)k / (NV - 1), a.ref_x0) : 0.0;
+    const double crefy = (k < NV) ? fma(a.ref_dy, (double)k / (NV - 1), a.ref_y0) : 0.0;
     double xiX = 0.0, xiY = 0.0, lamX = 0.0, lamY = 0.0, xi2r = 0.0, lamp = 0.0;
     const float* ini = a.init + l * 3 * NV;
     if (k < NV) {   // step 1: xi2 from the input, copies start at 0 (G15)
@@ -419,7 +526,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
       if (k < NV) lamp = li[2 * NV2 + k];
     }
     auto publish_xi1 = [&]() {
-      if (k < NV) { ws->cf[0][k] = (float)xiX; ws->cf[2][k] = (float)xiY; }
+      if (k < NV) { ws->cf[0][k] = (float)(xiX - crefx); ws->cf[2][k] = (float)(xiY - crefy); }
       else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
       if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
     };
@@ -427,15 +534,16 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
     if (k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
     __syncwarp();
 
-    float cr[NT], sr[NT], th[NT];
     float r1sq = 0.f, rpsq = 0.f;
     const bool trace = a.res_trace != nullptr;
     // initialisation of xi3, xi4 / g on the initial trajectory (G15)
-    phase_theta<NT>(Pt, QP, ws, lane, cr, sr, th);
-    if (K == 0) phase_project<NT, M, true>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
-    else phase_project<NT, M, false>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+    phase_theta(Pt, QP, ws, lane);
+    __syncwarp();
+    if (K == 0) phase_project<M, true>(pa, ws, lane, &r1sq, &rpsq);
+    else phase_project<M, false>(pa, ws, lane, &r1sq, &rpsq);
     __syncwarp();
 
+#pragma unroll 1
     for (int it = 0; it < K; ++it) {
       // ---- A: xi1 step -----------------------------------------------------
       if (k < NV2) {
@@ -463,7 +571,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
       publish_xi1();
       __syncwarp();
       // ---- B: heading target ----------------------------------------------
-      phase_theta<NT>(Pt, QP, ws, lane, cr, sr, th);
+      phase_theta(Pt, QP, ws, lane);
       __syncwarp();
       // ---- C: xi2 step + lambda_psi ------------------------------------------
       if (k < NV) ws->rhsp[k] = lamp + rho_psi * (double)ws->pth[k];
@@ -484,16 +592,15 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
         lamp -= gs - rho_psi * (double)ws->pth[k];
       }
       // ---- D: projections + contraction -------------------------------------
-      const bool want_res = trace || (it == K - 1);
-      if (want_res) phase_project<NT, M, true>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
-      else phase_project<NT, M, false>(a, Pt, obs, abi, ws, lane, cr, sr, th, r1sq, rpsq);
+      if (trace || it == K - 1) phase_project<M, true>(pa, ws, lane, &r1sq, &rpsq);
+      else phase_project<M, false>(pa, ws, lane, &r1sq, &rpsq);
       __syncwarp();
       // ---- E: multipliers ------------------------------------------------------
       if (k < NV2) {
         lamX -= rho * (double)ws->h[k];
         lamY -= rho * (double)ws->h[NV2 + k];
       }
-      if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(r1sq);
+      if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
     }
 
     // ---- outputs ------------------------------------------------------------
@@ -502,10 +609,10 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
       double gx = 0.0, gy = 0.0, gp = 0.0;
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
-        const double g = sf[BlobLayout::Gdd + j * NV + k];
-        gx = fma(g, ws->xi1[2 * j], gx);
-        gy = fma(g, ws->xi1[2 * j + 1], gy);
-        gp = fma(g, ws->xi2[j], gp);
+        const double gg = sf[BlobLayout::Gdd + j * NV + k];
+        gx = fma(gg, ws->xi1[2 * j], gx);
+        gy = fma(gg, ws->xi1[2 * j + 1], gy);
+        gp = fma(gg, ws->xi2[j], gp);
       }
       jpart = gx * xiX + gy * xiY + gp * xi2r;
     }
@@ -519,7 +626,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
       if (k < NV) lo[2 * NV2 + k] = (float)lamp;
     }
     if (lane == 0) {
-      const float r1 = sqrtf(r1sq), rp = sqrtf(rpsq);
+      const float r1 = sqrtf(fmaxf(r1sq, 0.f)), rp = sqrtf(rpsq);
       a.residual[2 * l] = r1;
       a.residual[2 * l + 1] = rp;
       a.cost[l] = (float)J;
@@ -555,20 +662,6 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const KernelArgs a) {
   }
 }
 
-template <int NT, int M>
-cudaError_t launch_t(const KernelArgs& a, int wpc, size_t smem, cudaStream_t s) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<NT, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  const unsigned grid = (unsigned)((a.B + wpc - 1) / wpc);
-  bmc_am_kernel<NT, M><<<grid, 32 * wpc, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 size_t kernel_smem_bytes(int QP, int n, int wpc);
@@ -577,14 +670,17 @@ size_t kernel_smem_bytes(int QP, int n, int wpc);
 // this; bmc_launch.cu dispatches on m.
 template <int M>
 cudaError_t launch_am_m(const KernelArgs& a, int wpc, cudaStream_t s) {
-  const size_t smem = smem_bytes(a.QP, a.n, wpc);
-  switch (a.NT) {
-    case 1: return launch_t<1, M>(a, wpc, smem, s);
-    case 2: return launch_t<2, M>(a, wpc, smem, s);
-    case 3: return launch_t<3, M>(a, wpc, smem, s);
-    case 4: return launch_t<4, M>(a, wpc, smem, s);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
   }
-  return cudaErrorInvalidValue;
+  const size_t smem = smem_bytes(a.QP, a.n, wpc);
+  const unsigned grid = (unsigned)((a.B + wpc - 1) / wpc);
+  bmc_am_kernel<M><<<grid, 32 * wpc, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace bmc

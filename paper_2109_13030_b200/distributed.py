@@ -1,0 +1,69 @@
+"""Sharded multi-GPU solve: one process per GPU, torch.distributed for plumbing.
+
+The batch is split into contiguous shards (rank r owns global instances
+[r B, (r+1) B), bmc_problem.index_base = r B); every rank builds the same
+scene from the seed, so there is no broadcast.  The only data-path collective
+is the best-of-batch exchange: each rank packs {key, 55 coefficients} of its
+shard's best into a 256-byte record (bmc_pack_best, our kernel), the records
+are all-gathered (NCCL over NVLink on GPUs, gloo in the CPU tests), and every
+rank selects the minimum key (bmc_select_best, our kernel), so all ranks hold
+the same global best.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+from .bmc import _check, load_library
+
+RECORD_WORDS = 32
+
+
+class BestExchange:
+    """Best-of-batch exchange over a process group.
+
+    `pack` / `select` default to the library's device kernels; the CPU tests
+    (gloo) inject host implementations to exercise the collective plumbing."""
+
+    def __init__(self, group, device, pack: Optional[Callable] = None, select: Optional[Callable] = None):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.device = device
+        self.record = torch.zeros(RECORD_WORDS, dtype=torch.int64, device=device)
+        self.records = torch.zeros(self.world * RECORD_WORDS, dtype=torch.int64, device=device)
+        self.best = torch.zeros(2, dtype=torch.int64, device=device)
+        self.coeffs = torch.zeros(55, dtype=torch.float32, device=device)
+        self._pack = pack or self._pack_device
+        self._select = select or self._select_device
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _pack_device(self, best, coeffs, index_base, record):
+        _check(load_library().bmc_pack_best(C.c_void_p(best.data_ptr()), C.c_void_p(coeffs.data_ptr()),
+                                            C.c_int64(index_base), C.c_void_p(record.data_ptr()),
+                                            self._stream()))
+
+    def _select_device(self, records, nranks, best_out, coeffs_out):
+        _check(load_library().bmc_select_best(C.c_void_p(records.data_ptr()), C.c_int32(nranks),
+                                              C.c_void_p(best_out.data_ptr()),
+                                              C.c_void_p(coeffs_out.data_ptr()), self._stream()))
+
+    def exchange(self, best, coeffs, index_base: int):
+        """best: [2] int64 of this shard's solve; coeffs: [B, 5, 11] of this shard.
+        Returns (global best [2], best coefficients [55]) on every rank."""
+        import torch.distributed as dist
+        self._pack(best, coeffs, index_base, self.record)
+        dist.all_gather_into_tensor(self.records, self.record, group=self.group)
+        self._select(self.records, self.world, self.best, self.coeffs)
+        return self.best, self.coeffs
+
+
+def shard_bounds(global_batch: int, world: int, rank: int):
+    """Contiguous shard of rank `rank`: (start, size), ceil(B / world) per rank."""
+    per = -(-global_batch // world)
+    start = min(rank * per, global_batch)
+    return start, max(0, min(per, global_batch - start))
