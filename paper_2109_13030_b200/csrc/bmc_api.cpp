@@ -123,7 +123,7 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
   c->r.assign(params->r, params->r + params->m);
   c->p.r = c->r.data();
   c->q = params->q;
-  c->QP = ((params->q + 31) / 32) * 32;
+  c->QP = Q_MAX;   // fixed sample stride of the shared-memory layout
   c->NT = c->QP / 32;
   {
     HostConsts hc;

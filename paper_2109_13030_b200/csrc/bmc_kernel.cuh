@@ -41,6 +41,8 @@ namespace bmc {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int QP = Q_MAX;   // sample stride of every per-sample smem array
+constexpr int JB = 8;       // obstacles per inside-test block
 
 struct WarpSmem {
   double xi1[2 * NV2];  // [k][ch]
@@ -50,14 +52,18 @@ struct WarpSmem {
   float cf[5][12];      // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s, c_psi (padded)
   float h[48];
   float pth[16];
-  float c[Q_MAX], s[Q_MAX], th[Q_MAX];   // copies c, s and theta per sample
+  float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
 };
 static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
 
 constexpr int U_DOUBLES = 56;  // u_x[22], u_y[22], u_psi[11] (+pad)
 
-__host__ __device__ inline size_t smem_bytes(int QP, int n, int wpc) {
-  return BlobLayout::bytes(QP) + (size_t)n * QP * sizeof(float2) + (size_t)n * sizeof(float4) +
+// obstacles are padded to a multiple of JB with far-away, zero-radius dummies
+__host__ __device__ inline int pad_obstacles(int n) { return (n + JB - 1) / JB * JB; }
+
+__host__ __device__ inline size_t smem_bytes(int n, int wpc) {
+  const int np = pad_obstacles(n);
+  return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
          U_DOUBLES * sizeof(double) + (size_t)wpc * sizeof(WarpSmem) + 16;
 }
 
@@ -147,20 +153,15 @@ __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
   c[8] = d.x; c[9] = d.y; c[10] = d.z;
 }
 
-// Round u of the sample loop: sample t, obstacle group g of S groups, R lanes per group.
-struct Round {
-  int t, g, S, R;
+// Per-kernel constants of the projection phase (registers / constant bank).
+struct Proj {
+  const float* Pt;       // smem basis [3][11][QP]
+  const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
+  const float4* abi;     // smem (a, b, a^2 or ab, kind) per obstacle
+  int q, n, ntf, rtail, rounds;
+  bool all_circ;
+  float nR1, nR2p1, v_max, a_max, vref_x, vref_y;
 };
-__device__ __forceinline__ Round make_round(int u, int ntf, int rtail, int lane) {
-  Round r;
-  if (u < ntf) {
-    r.t = 32 * u + lane; r.g = 0; r.S = 1; r.R = 32;
-  } else {
-    r.R = rtail; r.S = 32 / rtail;
-    r.t = 32 * ntf + (lane & (rtail - 1)); r.g = lane / rtail;
-  }
-  return r;
-}
 
 // --------------------------------------------------- collision projections
 // For every obstacle j of the lane's group and circle i at sample t:
@@ -171,94 +172,104 @@ __device__ __forceinline__ Round make_round(int u, int ntf, int rtail, int lane)
 //   kind 1 (literal atan2(y~,x~)): delta = (x~ (a f - 1), y~ (b f - 1)),
 //                                  f = max(1/rho, (a x~^2 + b y~^2)/(a^2 x~^2 + b^2 y~^2))
 //   kind 2 (scaled, G8):           delta = (x~, y~) max(ab / sqrt(b^2 x~^2 + a^2 y~^2) - 1, 0)
-// For kind 0, delta = 0 unless |(x~,y~)| < a: the rsqrt path runs only when
-// some lane of the warp is inside (warp-uniform branch).  The residual terms
-// (r_i e - delta)^2 are accumulated as base + delta (delta - 2 r_i e).
-// GUARD handles x~ = y~ = 0 exactly (G18: alpha = 0, d = 1 -> delta = (a, 0)).
-// SPLIT (tail round): lanes of different groups visit different obstacles, so
-// the trip count is made uniform with far-away dummy obstacles and the vote
-// runs over the active mask.
-template <int M, bool RES, bool GUARD, bool SPLIT>
-__device__ __forceinline__ void coll_loop(const float2* __restrict__ ob, const float4* __restrict__ abi,
-                                          int n, int QP, int g, int S, const float (&X)[M],
-                                          const float (&Y)[M], const float (&rec)[M], const float (&res_s)[M],
-                                          float (&Dx)[M], float (&Dy)[M], float& rc) {
+// The residual terms (r_i e - delta)^2 are accumulated as
+// base + delta (delta - 2 r_i e), with base = sum_i (r_i e)^2 per obstacle.
+//
+// Circular obstacles: delta = 0 unless |(x~, y~)| < a, so blocks of JB
+// obstacles are first tested (x~, y~, |.|^2 only); a warp-wide OR of the
+// per-lane inside masks selects the obstacles whose closed form (rsqrt on
+// the MUFU pipe) must run.  In the split tail round lanes of different groups
+// visit different obstacles, so trip counts are made uniform with empty
+// slots.
+template <int M, bool RES, bool SPLIT>
+__device__ __forceinline__ void coll_circ(const float2* __restrict__ ob, const float4* __restrict__ abi,
+                                          int n, int g, int S, const float (&X)[M], const float (&Y)[M],
+                                          const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
+                                          float (&Dy)[M], float& rc) {
   const int trips = SPLIT ? (n + S - 1) / S : n;
-#pragma unroll 2
-  for (int it = 0; it < trips; ++it) {
-    float2 o;
-    float4 ab;
-    if (SPLIT) {
-      const int j = g + it * S;
-      const bool have = j < n;
-      o = ob[(size_t)(have ? j : 0) * QP];
-      ab = abi[have ? j : 0];
-      if (!have) { o = make_float2(1.0e4f, 1.0e4f); ab = make_float4(1.f, 1.f, 1.f, 0.f); }
-    } else {
-      o = ob[(size_t)it * QP];
-      ab = abi[it];
-    }
-    if (ab.w == 0.f) {
-      float xt[M], yt[M], r2[M];
+#pragma unroll 1
+  for (int jb = 0; jb < trips; jb += JB) {
+    unsigned mask = 0;
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      const int it = jb + jj;
+      const int j = SPLIT ? g + it * S : it;   // unsplit: the padding makes every slot valid
+      const bool have = !SPLIT || ((it < trips) && (j < n));
+      const int jc = have ? j : 0;
+      const float2 o = ob[jc * QP];
+      const float a2 = abi[jc].z;
       float rmin = 3.0e38f;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
-        xt[i] = X[i] - o.x;
-        yt[i] = Y[i] - o.y;
-        r2[i] = fmaf(yt[i], yt[i], xt[i] * xt[i]);
-        rmin = fminf(rmin, r2[i]);
+        const float xt = X[i] - o.x, yt = Y[i] - o.y;
+        rmin = fminf(rmin, fmaf(yt, yt, xt * xt));
       }
-      if (__any_sync(SPLIT ? __activemask() : FULL, rmin < ab.z)) {
+      if (have && rmin < a2) mask |= 1u << jj;
+    }
+    unsigned need = __reduce_or_sync(FULL, mask);
+    while (need) {
+      const int jj = __ffs(need) - 1;
+      need &= need - 1;
+      const int it = jb + jj;
+      const int j = SPLIT ? g + it * S : it;
+      if ((mask >> jj) & 1u) {
+        const float2 o = ob[j * QP];
+        const float a = abi[j].x;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-          const float sc = fmaxf(fmaf(ab.x, rsqrt_ftz(r2[i]), -1.f), 0.f);
-          float dx = sc * xt[i], dy = sc * yt[i];
-          if (GUARD && r2[i] == 0.f) { dx = ab.x; dy = 0.f; }
+          const float xt = X[i] - o.x, yt = Y[i] - o.y;
+          const float sc = fmaxf(fmaf(a, rsqrt_ftz(fmaf(yt, yt, xt * xt)), -1.f), 0.f);
+          const float dx = sc * xt, dy = sc * yt;
           Dx[i] += dx;
           Dy[i] += dy;
           if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
         }
       }
-    } else {
-      const float a = ab.x, b = ab.y;
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const float xt = X[i] - o.x, yt = Y[i] - o.y;
-        const float x2 = xt * xt, y2 = yt * yt;
-        float dx, dy;
-        if (ab.w == 1.f) {
-          const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
-          const float f = fmaxf(rsqrt_ftz(x2 + y2), __fdividef(N, D));
-          dx = xt * fmaf(a, f, -1.f);
-          dy = yt * fmaf(b, f, -1.f);
-        } else {
-          const float R2 = fmaf(a * a, y2, b * b * x2);
-          const float sc = fmaxf(fmaf(ab.z, rsqrt_ftz(R2), -1.f), 0.f);
-          dx = sc * xt;
-          dy = sc * yt;
-        }
-        if (GUARD && x2 + y2 == 0.f) { dx = a; dy = 0.f; }
-        Dx[i] += dx;
-        Dy[i] += dy;
-        if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
-      }
     }
   }
 }
 
-template <int M, bool RES>
-__device__ __noinline__ void coll_loop_guarded(const float2* __restrict__ ob, const float4* __restrict__ abi,
-                                               int n, int QP, int g, int S, const float (&X)[M],
-                                               const float (&Y)[M], const float (&rec)[M],
-                                               const float (&res_s)[M], float (&Dx)[M], float (&Dy)[M],
-                                               float& rc) {
-  coll_loop<M, RES, true, true>(ob, abi, n, QP, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+// Any obstacle kinds, one obstacle at a time.  GUARD handles x~ = y~ = 0
+// exactly (G18: alpha = 0, d = 1 -> delta = (a, 0)).
+template <int M, bool RES, bool GUARD>
+__device__ __forceinline__ void coll_general(const float2* __restrict__ ob, const float4* __restrict__ abi,
+                                             int n, int g, int S, const float (&X)[M], const float (&Y)[M],
+                                             const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
+                                             float (&Dy)[M], float& rc) {
+#pragma unroll 1
+  for (int j = g; j < n; j += S) {
+    const float2 o = ob[j * QP];
+    const float4 ab = abi[j];
+    const float a = ab.x, b = ab.y;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const float xt = X[i] - o.x, yt = Y[i] - o.y;
+      const float x2 = xt * xt, y2 = yt * yt;
+      float dx, dy;
+      if (ab.w == 1.f) {
+        const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
+        const float f = fmaxf(rsqrt_ftz(x2 + y2), __fdividef(N, D));
+        dx = xt * fmaf(a, f, -1.f);
+        dy = yt * fmaf(b, f, -1.f);
+      } else {
+        const float R2 = (ab.w == 0.f) ? x2 + y2 : fmaf(a * a, y2, b * b * x2);
+        const float num = (ab.w == 0.f) ? a : ab.z;
+        const float sc = fmaxf(fmaf(num, rsqrt_ftz(R2), -1.f), 0.f);
+        dx = sc * xt;
+        dy = sc * yt;
+      }
+      if (GUARD && x2 + y2 == 0.f) { dx = a; dy = 0.f; }
+      Dx[i] += dx;
+      Dy[i] += dy;
+      if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
+    }
+  }
 }
 
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
-__device__ __noinline__ void phase_theta(const float* __restrict__ Pt, int QP, WarpSmem* ws, int lane) {
+__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSmem* ws, int lane, int q) {
   float cc[NV], cs[NV];
   load12(ws->cf[1], cc);
   load12(ws->cf[3], cs);
@@ -266,7 +277,7 @@ __device__ __noinline__ void phase_theta(const float* __restrict__ Pt, int QP, W
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.f;
 #pragma unroll 1
-  for (int t = lane; t < QP; t += 32) {
+  for (int t = lane; t < ((q + 31) & ~31); t += 32) {
     float p[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
@@ -287,20 +298,11 @@ __device__ __noinline__ void phase_theta(const float* __restrict__ Pt, int QP, W
   if (!(lane & 1) && (lane >> 1) < NV) ws->pth[lane >> 1] = v;
 }
 
-struct ProjArgs {
-  const float* Pt;
-  const float2* obs;
-  const float4* abi;
-  int QP, q, n, ntf, rtail, rounds;
-  float r[M_MAX];
-  float nR1, nR2p1, v_max, a_max, vref_x, vref_y;
-};
-
 // ---------------------------------------------------------------- phase D
 template <int M, bool RES>
-__device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int lane, float* res_out,
-                                           float* rpsi_out) {
-  const int QP = pa.QP, q = pa.q, n = pa.n;
+__device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws, int lane,
+                                              float& res_out, float& rpsi_out) {
+  const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float acc[48];
 #pragma unroll
@@ -308,9 +310,14 @@ __device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int
   float res = 0.f, rps = 0.f;
 #pragma unroll 1
   for (int u = 0; u < pa.rounds; ++u) {
-    const Round rd = make_round(u, pa.ntf, pa.rtail, lane);
-    const int t = rd.t;
-    const bool own = (rd.g == 0);               // group 0 owns the sample's contributions
+    int t, g, S, R;
+    if (u < pa.ntf) {
+      t = 32 * u + lane; g = 0; S = 1; R = 32;
+    } else {   // split tail round
+      R = pa.rtail; S = 32 / R;
+      t = 32 * pa.ntf + (lane & (R - 1)); g = lane / R;
+    }
+    const bool own = (g == 0);               // group 0 owns the sample's contributions
     const bool valid = own && (t < q);
     float x = 0.f, y = 0.f, xd = pa.vref_x, yd = pa.vref_y, xdd = 0.f, ydd = 0.f, psi = 0.f;
     {
@@ -354,18 +361,22 @@ __device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int
     float base = 0.f;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      X[i] = fmaf(pa.r[i], cps, x);
-      Y[i] = fmaf(pa.r[i], sp, y);
+      X[i] = fmaf(r[i], cps, x);
+      Y[i] = fmaf(r[i], sp, y);
       Dx[i] = 0.f;
       Dy[i] = 0.f;
-      rec[i] = pa.r[i] * ec;
-      res_s[i] = pa.r[i] * es;
+      rec[i] = r[i] * ec;
+      res_s[i] = r[i] * es;
       base = fmaf(rec[i], rec[i], fmaf(res_s[i], res_s[i], base));
     }
     float rc = 0.f;
     const float2* ob = pa.obs + t;
-    if (rd.S == 1) coll_loop<M, RES, false, false>(ob, pa.abi, n, QP, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
-    else coll_loop<M, RES, false, true>(ob, pa.abi, n, QP, rd.g, rd.S, X, Y, rec, res_s, Dx, Dy, rc);
+    if (pa.all_circ) {
+      if (S == 1) coll_circ<M, RES, false>(ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
+      else coll_circ<M, RES, true>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+    } else {
+      coll_general<M, RES, false>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+    }
     float chk = rc;
 #pragma unroll
     for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
@@ -373,9 +384,9 @@ __device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int
 #pragma unroll
       for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
       rc = 0.f;
-      coll_loop_guarded<M, RES>(ob, pa.abi, n, QP, rd.g, rd.S, X, Y, rec, res_s, Dx, Dy, rc);
+      coll_general<M, RES, true>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     }
-    for (int off = rd.R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
+    for (int off = R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         Dx[i] += __shfl_xor_sync(FULL, Dx[i], off);
@@ -388,8 +399,8 @@ __device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int
     for (int i = 0; i < M; ++i) {
       Ds_x += Dx[i];
       Ds_y += Dy[i];
-      Ex = fmaf(pa.r[i], Dx[i], Ex);
-      Ey = fmaf(pa.r[i], Dy[i], Ey);
+      Ex = fmaf(r[i], Dx[i], Ex);
+      Ey = fmaf(r[i], Dy[i], Ey);
     }
     const float w = own ? 1.f : 0.f;
     const float u1x = w * fmaf(pa.nR1, ec, -Ds_x), u1y = w * fmaf(pa.nR1, es, -Ds_y);
@@ -413,8 +424,8 @@ __device__ __noinline__ void phase_project(const ProjArgs& pa, WarpSmem* ws, int
   ws->h[lane] = v32;
   if (!(lane & 1)) ws->h[32 + (lane >> 1)] = v16;
   if (RES) {
-    *res_out = warp_sum(res);
-    *rpsi_out = warp_sum(rps);
+    res_out = warp_sum(res);
+    rpsi_out = warp_sum(rps);
   }
 }
 
@@ -423,12 +434,13 @@ template <int M>
 __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
-  const int QP = a.QP, n = a.n, q = a.q, K = a.iters;
+  const int n = a.n, q = a.q, K = a.iters;
   const double* sf = reinterpret_cast<const double*>(smem);
   const float* Pt = reinterpret_cast<const float*>(smem + BlobLayout::bytes_f64);
   float2* obs = reinterpret_cast<float2*>(smem + BlobLayout::bytes(QP));
-  float4* abi = reinterpret_cast<float4*>(obs + (size_t)n * QP);
-  double* ub = reinterpret_cast<double*>(abi + n);
+  const int npad = pad_obstacles(n);
+  float4* abi = reinterpret_cast<float4*>(obs + (size_t)npad * QP);
+  double* ub = reinterpret_cast<double*>(abi + npad);
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
   WarpSmem* ws = wsbase + warp;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(wsbase + wpc);
@@ -448,45 +460,48 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
   // obstacles relative to the boundary line (x_ref(t), y_ref(t)), computed in
   // fp64 and rounded once; padding samples far away
   const double inv_q1 = 1.0 / (double)(q - 1);
-  for (int idx = tid; idx < n * QP; idx += blockDim.x) {
+  for (int idx = tid; idx < npad * QP; idx += blockDim.x) {
     const int j = idx / QP, t = idx - j * QP;
     float2 v = make_float2(1.0e4f, 1.0e4f);
-    if (t < q) {
+    if (t < q && j < n) {
       const double tau = (double)t * inv_q1;
       v = make_float2((float)((double)__ldg(a.obs_xy + (size_t)(2 * j) * q + t) - fma(a.ref_dx, tau, a.ref_x0)),
                       (float)((double)__ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t) - fma(a.ref_dy, tau, a.ref_y0)));
     }
     obs[idx] = v;
   }
+  int circ = 1;
+  for (int j = n + tid; j < npad; j += blockDim.x) abi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
     abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
+    circ &= (aa == bb);
   }
   for (int i = tid; i < wpc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
+  const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
   __syncthreads();
   if (tid < NV2) {   // u = K12 b per channel (boundary part of Eq. 4)
     double sx = 0.0, sy = 0.0;
-    for (int r = 0; r < a.nb; ++r) {
-      sx = fma(sf[BlobLayout::K12t + r * NV2 + tid], a.b[0][r], sx);
-      sy = fma(sf[BlobLayout::K12t + r * NV2 + tid], a.b[1][r], sy);
+    for (int rr = 0; rr < a.nb; ++rr) {
+      sx = fma(sf[BlobLayout::K12t + rr * NV2 + tid], a.b[0][rr], sx);
+      sy = fma(sf[BlobLayout::K12t + rr * NV2 + tid], a.b[1][rr], sy);
     }
     ub[tid] = sx;
     ub[NV2 + tid] = sy;
     if (tid < NV) {
       double s = 0.0;
-      for (int r = 0; r < a.nb; ++r) s = fma(sf[BlobLayout::Kp12t + r * NV + tid], a.b[2][r], s);
+      for (int rr = 0; rr < a.nb; ++rr) s = fma(sf[BlobLayout::Kp12t + rr * NV + tid], a.b[2][rr], s);
       ub[2 * NV2 + tid] = s;
     }
   }
   __syncthreads();
 
-  ProjArgs pa;
+  Proj pa;
   pa.Pt = Pt;
   pa.obs = obs;
   pa.abi = abi;
-  pa.QP = QP;
   pa.q = q;
   pa.n = n;
   pa.ntf = q / 32;
@@ -497,14 +512,16 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
     pa.rtail = R;
     pa.rounds = pa.ntf + (rem > 0 ? 1 : 0);
   }
-#pragma unroll
-  for (int i = 0; i < M_MAX; ++i) pa.r[i] = a.r[i];
+  pa.all_circ = all_circ;
   pa.nR1 = a.nR1;
   pa.nR2p1 = a.nR2p1;
   pa.v_max = a.v_max;
   pa.a_max = a.a_max;
   pa.vref_x = (float)(a.ref_dx / a.T);
   pa.vref_y = (float)(a.ref_dy / a.T);
+  float r[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) r[i] = a.r[i];
 
   const long long l = (long long)blockIdx.x * wpc + warp;
   if (l < a.B) {
@@ -525,82 +542,78 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
       if (k < NV2) { lamX = li[k]; lamY = li[NV2 + k]; }
       if (k < NV) lamp = li[2 * NV2 + k];
     }
-    auto publish_xi1 = [&]() {
-      if (k < NV) { ws->cf[0][k] = (float)(xiX - crefx); ws->cf[2][k] = (float)(xiY - crefy); }
-      else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
-      if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
-    };
-    publish_xi1();
     if (k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
-    __syncwarp();
 
     float r1sq = 0.f, rpsq = 0.f;
     const bool trace = a.res_trace != nullptr;
-    // initialisation of xi3, xi4 / g on the initial trajectory (G15)
-    phase_theta(Pt, QP, ws, lane);
-    __syncwarp();
-    if (K == 0) phase_project<M, true>(pa, ws, lane, &r1sq, &rpsq);
-    else phase_project<M, false>(pa, ws, lane, &r1sq, &rpsq);
-    __syncwarp();
-
+    // it = -1 is the initialisation of xi3, xi4 / g on the initial trajectory
+    // (G15); every phase has a single call site so each is inlined once.
 #pragma unroll 1
-    for (int it = 0; it < K; ++it) {
-      // ---- A: xi1 step -----------------------------------------------------
-      if (k < NV2) {
-        ws->rhs[2 * k] = lamX - rho * (double)ws->h[k];
-        ws->rhs[2 * k + 1] = lamY - rho * (double)ws->h[NV2 + k];
-      }
-      __syncwarp();
-      if (k < NV2) {
-        double ax = ub[k], ay = ub[NV2 + k], bx = 0.0, by = 0.0;
-#pragma unroll 11
-        for (int j = 0; j < NV2; ++j) {
-          const double mkj = sf[BlobLayout::Mt + j * NV2 + k];
-          const double kkj = sf[BlobLayout::K11t + j * NV2 + k];
-          const double2 xj = reinterpret_cast<const double2*>(ws->xi1)[j];
-          const double2 rj = reinterpret_cast<const double2*>(ws->rhs)[j];
-          ax = fma(mkj, xj.x, ax);
-          ay = fma(mkj, xj.y, ay);
-          bx = fma(kkj, rj.x, bx);
-          by = fma(kkj, rj.y, by);
+    for (int it = -1; it < K; ++it) {
+      if (it >= 0) {
+        // ---- A: xi1 step ---------------------------------------------------
+        if (k < NV2) {
+          ws->rhs[2 * k] = lamX - rho * (double)ws->h[k];
+          ws->rhs[2 * k + 1] = lamY - rho * (double)ws->h[NV2 + k];
         }
-        xiX = ax + bx;
-        xiY = ay + by;
+        __syncwarp();
+        if (k < NV2) {
+          double ax = ub[k], ay = ub[NV2 + k], bx = 0.0, by = 0.0;
+#pragma unroll 11
+          for (int j = 0; j < NV2; ++j) {
+            const double mkj = sf[BlobLayout::Mt + j * NV2 + k];
+            const double kkj = sf[BlobLayout::K11t + j * NV2 + k];
+            const double2 xj = reinterpret_cast<const double2*>(ws->xi1)[j];
+            const double2 rj = reinterpret_cast<const double2*>(ws->rhs)[j];
+            ax = fma(mkj, xj.x, ax);
+            ay = fma(mkj, xj.y, ay);
+            bx = fma(kkj, rj.x, bx);
+            by = fma(kkj, rj.y, by);
+          }
+          xiX = ax + bx;
+          xiY = ay + by;
+        }
+        __syncwarp();
       }
+      if (k < NV) { ws->cf[0][k] = (float)(xiX - crefx); ws->cf[2][k] = (float)(xiY - crefy); }
+      else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
+      if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
       __syncwarp();
-      publish_xi1();
+      // ---- B: heading target ------------------------------------------------
+      phase_theta(Pt, ws, lane, q);
       __syncwarp();
-      // ---- B: heading target ----------------------------------------------
-      phase_theta(Pt, QP, ws, lane);
-      __syncwarp();
-      // ---- C: xi2 step + lambda_psi ------------------------------------------
-      if (k < NV) ws->rhsp[k] = lamp + rho_psi * (double)ws->pth[k];
-      __syncwarp();
-      if (k < NV) {
-        double s = ub[2 * NV2 + k];
+      if (it >= 0) {
+        // ---- C: xi2 step + lambda_psi ----------------------------------------
+        if (k < NV) ws->rhsp[k] = lamp + rho_psi * (double)ws->pth[k];
+        __syncwarp();
+        if (k < NV) {
+          double s = ub[2 * NV2 + k];
 #pragma unroll
-        for (int j = 0; j < NV; ++j) s = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhsp[j], s);
-        xi2r = s;
-        ws->xi2[k] = s;
-        ws->cf[4][k] = (float)s;
-      }
-      __syncwarp();
-      if (k < NV) {
-        double gs = 0.0;
+          for (int j = 0; j < NV; ++j) s = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhsp[j], s);
+          xi2r = s;
+          ws->xi2[k] = s;
+          ws->cf[4][k] = (float)s;
+        }
+        __syncwarp();
+        if (k < NV) {
+          double gs = 0.0;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) gs = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2[j], gs);
-        lamp -= gs - rho_psi * (double)ws->pth[k];
+          for (int j = 0; j < NV; ++j) gs = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2[j], gs);
+          lamp -= gs - rho_psi * (double)ws->pth[k];
+        }
       }
-      // ---- D: projections + contraction -------------------------------------
-      if (trace || it == K - 1) phase_project<M, true>(pa, ws, lane, &r1sq, &rpsq);
-      else phase_project<M, false>(pa, ws, lane, &r1sq, &rpsq);
+      // ---- D: projections + contraction ---------------------------------------
+      if (trace ? (it >= 0) : (it == K - 1)) phase_project<M, true>(pa, r, ws, lane, r1sq, rpsq);
+      else phase_project<M, false>(pa, r, ws, lane, r1sq, rpsq);
       __syncwarp();
-      // ---- E: multipliers ------------------------------------------------------
-      if (k < NV2) {
-        lamX -= rho * (double)ws->h[k];
-        lamY -= rho * (double)ws->h[NV2 + k];
+      if (it >= 0) {
+        // ---- E: multipliers ----------------------------------------------------
+        if (k < NV2) {
+          lamX -= rho * (double)ws->h[k];
+          lamY -= rho * (double)ws->h[NV2 + k];
+        }
+        if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
       }
-      if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
     }
 
     // ---- outputs ------------------------------------------------------------
@@ -664,7 +677,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
 
 }  // namespace
 
-size_t kernel_smem_bytes(int QP, int n, int wpc);
+size_t kernel_smem_bytes(int QPx, int n, int wpc);
 
 // One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
 // this; bmc_launch.cu dispatches on m.
@@ -677,7 +690,7 @@ cudaError_t launch_am_m(const KernelArgs& a, int wpc, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const size_t smem = smem_bytes(a.QP, a.n, wpc);
+  const size_t smem = smem_bytes(a.n, wpc);
   const unsigned grid = (unsigned)((a.B + wpc - 1) / wpc);
   bmc_am_kernel<M><<<grid, 32 * wpc, smem, s>>>(a);
   return cudaGetLastError();

@@ -79,7 +79,7 @@ bool lu_inverse(std::vector<double> a, int N, std::vector<double>& inv) {
 }  // namespace
 
 int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err) {
-  const int q = p.q, QP = ((q + 31) / 32) * 32, deg = NV - 1;
+  const int q = p.q, QP = Q_MAX, deg = NV - 1;  // fixed sample stride (compile-time in the kernel)
   out->q = q;
   out->QP = QP;
   out->n = n;
