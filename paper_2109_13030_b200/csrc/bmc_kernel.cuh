@@ -186,43 +186,58 @@ __device__ __forceinline__ void coll_circ(const float2* __restrict__ ob, const f
                                           int n, int g, int S, const float (&X)[M], const float (&Y)[M],
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                           float (&Dy)[M], float& rc) {
-  const int trips = SPLIT ? (n + S - 1) / S : n;
+  const int trips = SPLIT ? (n + S - 1) / S : pad_obstacles(n);
+  constexpr int NBK = 4;   // blocks per chunk: their REDUX.OR votes are issued back to back
 #pragma unroll 1
-  for (int jb = 0; jb < trips; jb += JB) {
-    unsigned mask = 0;
+  for (int jc0 = 0; jc0 < trips; jc0 += NBK * JB) {
+    unsigned mask[NBK];
 #pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int it = jb + jj;
-      const int j = SPLIT ? g + it * S : it;   // unsplit: the padding makes every slot valid
-      const bool have = !SPLIT || ((it < trips) && (j < n));
-      const int jc = have ? j : 0;
-      const float2 o = ob[jc * QP];
-      const float a2 = abi[jc].z;
-      float rmin = 3.0e38f;
+    for (int bk = 0; bk < NBK; ++bk) {
+      mask[bk] = 0u;
+      const int jb = jc0 + bk * JB;
+      if (jb < trips) {
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const float xt = X[i] - o.x, yt = Y[i] - o.y;
-        rmin = fminf(rmin, fmaf(yt, yt, xt * xt));
+        for (int jj = 0; jj < JB; ++jj) {
+          const int it = jb + jj;
+          const int j = SPLIT ? g + it * S : it;   // unsplit: the padding makes every slot valid
+          const bool have = !SPLIT || ((it < trips) && (j < n));
+          const int jcl = have ? j : 0;
+          const float2 o = ob[jcl * QP];
+          const float a2 = abi[jcl].z;
+          float rmin = 0.f;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            const float xt = X[i] - o.x, yt = Y[i] - o.y;
+            const float r2 = fmaf(yt, yt, xt * xt);
+            rmin = (i == 0) ? r2 : fminf(rmin, r2);
+          }
+          mask[bk] |= (have && rmin < a2) ? (1u << jj) : 0u;
+        }
       }
-      if (have && rmin < a2) mask |= 1u << jj;
     }
-    unsigned need = __reduce_or_sync(FULL, mask);
-    while (need) {
-      const int jj = __ffs(need) - 1;
-      need &= need - 1;
-      const int it = jb + jj;
-      const int j = SPLIT ? g + it * S : it;
-      if ((mask >> jj) & 1u) {
-        const float2 o = ob[j * QP];
-        const float a = abi[j].x;
+    unsigned need[NBK];
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-          const float xt = X[i] - o.x, yt = Y[i] - o.y;
-          const float sc = fmaxf(fmaf(a, rsqrt_ftz(fmaf(yt, yt, xt * xt)), -1.f), 0.f);
-          const float dx = sc * xt, dy = sc * yt;
-          Dx[i] += dx;
-          Dy[i] += dy;
-          if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
+    for (int bk = 0; bk < NBK; ++bk) need[bk] = __reduce_or_sync(FULL, mask[bk]);
+#pragma unroll
+    for (int bk = 0; bk < NBK; ++bk) {
+      unsigned nd = need[bk];
+      while (nd) {
+        const int jj = __ffs(nd) - 1;
+        nd &= nd - 1;
+        const int it = jc0 + bk * JB + jj;
+        const int j = SPLIT ? g + it * S : it;
+        if ((mask[bk] >> jj) & 1u) {
+          const float2 o = ob[j * QP];
+          const float a = abi[j].x;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            const float xt = X[i] - o.x, yt = Y[i] - o.y;
+            const float sc = fmaxf(fmaf(a, rsqrt_ftz(fmaf(yt, yt, xt * xt)), -1.f), 0.f);
+            const float dx = sc * xt, dy = sc * yt;
+            Dx[i] += dx;
+            Dy[i] += dy;
+            if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
+          }
         }
       }
     }
@@ -276,8 +291,11 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
   float acc[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.f;
-#pragma unroll 1
-  for (int t = lane; t < ((q + 31) & ~31); t += 32) {
+  const int nr = (q + 31) >> 5;
+#pragma unroll
+  for (int u = 0; u < QP / 32; ++u) {   // unrolled: independent atan2 chains overlap
+    if (u >= nr) break;
+    const int t = 32 * u + lane;
     float p[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
