@@ -4,8 +4,10 @@
 // (setup.cpp); every step of the iteration runs in bmc_kernel.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -236,10 +238,17 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   Blob* blob = nullptr;
   int32_t rc = get_blob(c, pr->n_obs, &blob);
   if (rc != BMC_OK) return rc;
-  int wpc = 4;
-  while (wpc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, wpc) > 227 * 1024) --wpc;
-  if (kernel_smem_bytes(c->QP, pr->n_obs, wpc) > 227 * 1024)
+  // launch shape: `team` warps per instance, `ipc` instances per CTA.  One
+  // warp per instance by default; BMC_TEAM / BMC_IPC override (experiments).
+  int team = 1, ipc = 4;
+  if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
+  if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
+  if (team < 1 || team > 4) team = 1;
+  if (ipc < 1 || ipc * team > 32) ipc = std::max(1, 4 / team);
+  while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024) --ipc;
+  if (kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024)
     return fail(BMC_EINVAL, "n_obs * q too large for shared memory");
+  const int wpc = ipc;   // launch_am takes instances per CTA
   KernelArgs a;
   std::memset(&a, 0, sizeof(a));
   a.blob = blob->d;
@@ -264,6 +273,7 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   a.m = c->p.m;
   a.nb = blob->nb;
   a.iters = pr->iters;
+  a.team = team;
   a.alpha_rule = c->p.alpha_rule;
   double R1 = 0.0, R2 = 0.0;
   for (int i = 0; i < c->p.m; ++i) {

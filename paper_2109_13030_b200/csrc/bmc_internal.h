@@ -59,6 +59,7 @@ struct KernelArgs {
   unsigned int* ws_count;
   long long B, index_base;
   int q, QP, NT, n, m, nb, iters, alpha_rule;
+  int team;                    // warps per instance (1..4); CTA = team * ipc warps
   float r[M_MAX];
   float nR1, nR2p1;            // n sum r_i, n sum r_i^2 + 1 (F^T F closed form)
   float v_max, a_max;

@@ -44,17 +44,32 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int QP = Q_MAX;   // sample stride of every per-sample smem array
 constexpr int JB = 8;       // obstacles per inside-test block
 
+constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per round
+
+// Per-instance state shared by the T warps of its team.
 struct WarpSmem {
   double xi1[2 * NV2];  // [k][ch]
   double rhs[2 * NV2];  // [k][ch]
   double xi2[12];
   double rhsp[12];
   float cf[5][12];      // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s, c_psi (padded)
-  float h[48];
-  float pth[16];
+  float h[48];          // F^T (F xi1 - g), summed over the team's warps
+  float pth[16];        // P^T theta, summed
   float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
+  float part_h[T_MAX][48];      // per-warp partials, summed in warp order (deterministic)
+  float part_th[T_MAX][16];
+  float part_res[T_MAX][4];
 };
 static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
+
+// Team barrier: named barrier per team (id 1 + team) over its 32 T threads.
+__device__ __forceinline__ void team_sync(int team, int T) {
+  if (T == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * T) : "memory");
+  }
+}
 
 constexpr int U_DOUBLES = 56;  // u_x[22], u_y[22], u_psi[11] (+pad)
 
@@ -284,7 +299,8 @@ __device__ __forceinline__ void coll_general(const float2* __restrict__ ob, cons
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
-__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSmem* ws, int lane, int q) {
+__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSmem* ws, int lane, int q,
+                                            int w, int T) {
   float cc[NV], cs[NV];
   load12(ws->cf[1], cc);
   load12(ws->cf[3], cs);
@@ -293,7 +309,8 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
   for (int k = 0; k < 16; ++k) acc[k] = 0.f;
   const int nr = (q + 31) >> 5;
 #pragma unroll
-  for (int u = 0; u < QP / 32; ++u) {   // unrolled: independent atan2 chains overlap
+  for (int uu = 0; uu < QP / 32; ++uu) {   // unrolled: independent atan2 chains overlap
+    const int u = w + uu * T;                // this warp's rounds within the team
     if (u >= nr) break;
     const int t = 32 * u + lane;
     float p[NV];
@@ -313,13 +330,13 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
     for (int k = 0; k < NV; ++k) acc[k] = fmaf(p[k], tht, acc[k]);
   }
   const float v = transpose_reduce16(acc, lane);
-  if (!(lane & 1) && (lane >> 1) < NV) ws->pth[lane >> 1] = v;
+  if (!(lane & 1) && (lane >> 1) < NV) ws->part_th[w][lane >> 1] = v;
 }
 
 // ---------------------------------------------------------------- phase D
 template <int M, bool RES>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws, int lane,
-                                              float& res_out, float& rpsi_out) {
+                                              int w, int T) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float acc[48];
@@ -327,7 +344,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   for (int k = 0; k < 48; ++k) acc[k] = 0.f;
   float res = 0.f, rps = 0.f;
 #pragma unroll 1
-  for (int u = 0; u < pa.rounds; ++u) {
+  for (int u = w; u < pa.rounds; u += T) {   // this warp's rounds within the team
     int t, g, S, R;
     if (u < pa.ntf) {
       t = 32 * u + lane; g = 0; S = 1; R = 32;
@@ -439,11 +456,15 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   }
   const float v32 = transpose_reduce32(acc, lane);
   const float v16 = transpose_reduce16(acc + 32, lane);
-  ws->h[lane] = v32;
-  if (!(lane & 1)) ws->h[32 + (lane >> 1)] = v16;
+  ws->part_h[w][lane] = v32;
+  if (!(lane & 1)) ws->part_h[w][32 + (lane >> 1)] = v16;
   if (RES) {
-    res_out = warp_sum(res);
-    rpsi_out = warp_sum(rps);
+    res = warp_sum(res);
+    rps = warp_sum(rps);
+    if (lane == 0) {
+      ws->part_res[w][0] = res;
+      ws->part_res[w][1] = rps;
+    }
   }
 }
 
@@ -460,8 +481,9 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
   float4* abi = reinterpret_cast<float4*>(obs + (size_t)npad * QP);
   double* ub = reinterpret_cast<double*>(abi + npad);
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
-  WarpSmem* ws = wsbase + warp;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(wsbase + wpc);
+  const int T = a.team, ipc = wpc / T;               // warps per instance, instances per CTA
+  const int team = warp / T, w = warp - team * T;    // instance slot in the CTA, rank in the team
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wsbase + ipc);
 
   // --- stage the batch-invariant data -------------------------------------
   if (tid == 0) mbar_init(mbar, 1);
@@ -496,7 +518,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
     abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
     circ &= (aa == bb);
   }
-  for (int i = tid; i < wpc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
+  for (int i = tid; i < ipc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
   const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
   __syncthreads();
@@ -541,8 +563,10 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
 
-  const long long l = (long long)blockIdx.x * wpc + warp;
-  if (l < a.B) {
+  WarpSmem* ws = wsbase + team;
+  const bool lead = (w == 0);   // the team leader owns the fp64 state and the dense steps
+  const long long l = (long long)blockIdx.x * ipc + team;
+  if (l < a.B && team < ipc) {
     const int k = lane;
     const double rho = a.rho, rho_psi = a.rho_psi;
     // Bernstein control points of the boundary line (linear precision: c_k = x0 + dx k / 10)
@@ -560,14 +584,17 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
       if (k < NV2) { lamX = li[k]; lamY = li[NV2 + k]; }
       if (k < NV) lamp = li[2 * NV2 + k];
     }
-    if (k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
+    if (lead && k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
 
     float r1sq = 0.f, rpsq = 0.f;
     const bool trace = a.res_trace != nullptr;
     // it = -1 is the initialisation of xi3, xi4 / g on the initial trajectory
     // (G15); every phase has a single call site so each is inlined once.
+    // Team protocol per iteration: leader A | all B | leader C | all D | leader E,
+    // separated by team barriers; partial sums are combined in warp order.
 #pragma unroll 1
     for (int it = -1; it < K; ++it) {
+      if (lead) {
       if (it >= 0) {
         // ---- A: xi1 step ---------------------------------------------------
         if (k < NV2) {
@@ -596,9 +623,17 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
       if (k < NV) { ws->cf[0][k] = (float)(xiX - crefx); ws->cf[2][k] = (float)(xiY - crefy); }
       else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
       if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
-      __syncwarp();
+      }
+      team_sync(team, T);
       // ---- B: heading target ------------------------------------------------
-      phase_theta(Pt, ws, lane, q);
+      phase_theta(Pt, ws, lane, q, w, T);
+      team_sync(team, T);
+      if (lead) {
+      if (k < NV) {
+        float s = 0.f;
+        for (int ww = 0; ww < T; ++ww) s += ws->part_th[ww][k];
+        ws->pth[k] = s;
+      }
       __syncwarp();
       if (it >= 0) {
         // ---- C: xi2 step + lambda_psi ----------------------------------------
@@ -620,19 +655,39 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
           lamp -= gs - rho_psi * (double)ws->pth[k];
         }
       }
+      }
+      team_sync(team, T);
       // ---- D: projections + contraction ---------------------------------------
-      if (trace ? (it >= 0) : (it == K - 1)) phase_project<M, true>(pa, r, ws, lane, r1sq, rpsq);
-      else phase_project<M, false>(pa, r, ws, lane, r1sq, rpsq);
-      __syncwarp();
-      if (it >= 0) {
-        // ---- E: multipliers ----------------------------------------------------
-        if (k < NV2) {
-          lamX -= rho * (double)ws->h[k];
-          lamY -= rho * (double)ws->h[NV2 + k];
+      const bool want_res = trace ? (it >= 0) : (it == K - 1);
+      if (want_res) phase_project<M, true>(pa, r, ws, lane, w, T);
+      else phase_project<M, false>(pa, r, ws, lane, w, T);
+      team_sync(team, T);
+      if (lead) {
+        for (int kk = lane; kk < 48; kk += 32) {
+          float s = 0.f;
+          for (int ww = 0; ww < T; ++ww) s += ws->part_h[ww][kk];
+          ws->h[kk] = s;
         }
-        if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
+        if (want_res) {
+          r1sq = 0.f;
+          rpsq = 0.f;
+          for (int ww = 0; ww < T; ++ww) {
+            r1sq += ws->part_res[ww][0];
+            rpsq += ws->part_res[ww][1];
+          }
+        }
+        __syncwarp();
+        if (it >= 0) {
+          // ---- E: multipliers --------------------------------------------------
+          if (k < NV2) {
+            lamX -= rho * (double)ws->h[k];
+            lamY -= rho * (double)ws->h[NV2 + k];
+          }
+          if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
+        }
       }
     }
+    if (lead) {
 
     // ---- outputs ------------------------------------------------------------
     double jpart = 0.0;
@@ -677,6 +732,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
       atomicMin(a.ws_key, key);
       __threadfence();
     }
+    }
   }
   // ---- grid-wide argmin: the last CTA publishes and resets the workspace ----
   __syncthreads();
@@ -700,7 +756,7 @@ size_t kernel_smem_bytes(int QPx, int n, int wpc);
 // One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
 // this; bmc_launch.cu dispatches on m.
 template <int M>
-cudaError_t launch_am_m(const KernelArgs& a, int wpc, cudaStream_t s) {
+cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -708,9 +764,9 @@ cudaError_t launch_am_m(const KernelArgs& a, int wpc, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const size_t smem = smem_bytes(a.n, wpc);
-  const unsigned grid = (unsigned)((a.B + wpc - 1) / wpc);
-  bmc_am_kernel<M><<<grid, 32 * wpc, smem, s>>>(a);
+  const size_t smem = smem_bytes(a.n, ipc);
+  const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
+  bmc_am_kernel<M><<<grid, 32 * a.team * ipc, smem, s>>>(a);
   return cudaGetLastError();
 }
 
