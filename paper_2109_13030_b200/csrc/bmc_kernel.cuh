@@ -59,6 +59,7 @@ struct WarpSmem {
   float part_h[T_MAX][48];      // per-warp partials, summed in warp order (deterministic)
   float part_th[T_MAX][16];
   float part_res[T_MAX][4];
+  float U[8][QP];               // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2)
 };
 static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
 
@@ -334,14 +335,17 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
 }
 
 // ---------------------------------------------------------------- phase D
+// D1 (per round): trajectory at the lane's sample, velocity / acceleration and
+// collision projections, and the per-sample vectors of h = F^T (F xi1 - g)
+//   U0 = n R1 e_c - D_x, U1 = (n R2 + 1) e_c - E_x, U2, U3 likewise for y,
+//   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
+// written to shared memory; D2: contraction with P, Pdot, Pddot.  Splitting
+// keeps the 44 contraction accumulators out of the obstacle loop's registers.
 template <int M, bool RES>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws, int lane,
                                               int w, int T) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
-  float acc[48];
-#pragma unroll
-  for (int k = 0; k < 48; ++k) acc[k] = 0.f;
   float res = 0.f, rps = 0.f;
 #pragma unroll 1
   for (int u = w; u < pa.rounds; u += T) {   // this warp's rounds within the team
@@ -362,33 +366,21 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       load12(ws->cf[4], cp);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        const float p = Pt[k * QP + t];
+        const float p = Pt[k * QP + t], pd = Pt[(NV + k) * QP + t], pdd = Pt[(2 * NV + k) * QP + t];
         x = fmaf(p, cx[k], x);
         y = fmaf(p, cy[k], y);
         psi = fmaf(p, cp[k], psi);
+        xd = fmaf(pd, cx[k], xd);
+        yd = fmaf(pd, cy[k], yd);
+        xdd = fmaf(pdd, cx[k], xdd);
+        ydd = fmaf(pdd, cy[k], ydd);
       }
-      float pd[NV], pdd[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        pd[k] = Pt[(NV + k) * QP + t];
-        pdd[k] = Pt[(2 * NV + k) * QP + t];
-        xd = fmaf(pd[k], cx[k], xd);
-        yd = fmaf(pd[k], cy[k], yd);
-        xdd = fmaf(pdd[k], cx[k], xdd);
-        ydd = fmaf(pdd[k], cy[k], ydd);
-      }
-      // velocity / acceleration: g = projection onto the bound disk (G6, G7)
-      const float sv = fminf(fmaf(pa.v_max, rsqrt_ftz(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
-      const float sa = fminf(fmaf(pa.a_max, rsqrt_ftz(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
-      const float w = own ? -1.f : 0.f;
-      const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        acc[k] = fmaf(pd[k], w * dvx, fmaf(pdd[k], w * dax, acc[k]));
-        acc[NV2 + k] = fmaf(pd[k], w * dvy, fmaf(pdd[k], w * day, acc[NV2 + k]));
-      }
-      if (RES && valid) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
     }
+    // velocity / acceleration: g = projection onto the bound disk (G6, G7)
+    const float sv = fminf(fmaf(pa.v_max, rsqrt_ftz(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
+    const float sa = fminf(fmaf(pa.a_max, rsqrt_ftz(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
+    const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
+    if (RES && valid) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
     float sp, cps;
     sincosf(psi, &sp, &cps);
     const float ec = ws->c[t] - cps, es = ws->s[t] - sp;
@@ -437,21 +429,39 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       Ex = fmaf(r[i], Dx[i], Ex);
       Ey = fmaf(r[i], Dy[i], Ey);
     }
-    const float w = own ? 1.f : 0.f;
-    const float u1x = w * fmaf(pa.nR1, ec, -Ds_x), u1y = w * fmaf(pa.nR1, es, -Ds_y);
-    const float vx = w * fmaf(pa.nR2p1, ec, -Ex), vy = w * fmaf(pa.nR2p1, es, -Ey);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const float p = Pt[k * QP + t];
-      acc[k] = fmaf(p, u1x, acc[k]);
-      acc[NV + k] = fmaf(p, vx, acc[NV + k]);
-      acc[NV2 + k] = fmaf(p, u1y, acc[NV2 + k]);
-      acc[NV2 + NV + k] = fmaf(p, vy, acc[NV2 + NV + k]);
+    if (own) {
+      ws->U[0][t] = fmaf(pa.nR1, ec, -Ds_x);
+      ws->U[1][t] = fmaf(pa.nR2p1, ec, -Ex);
+      ws->U[2][t] = fmaf(pa.nR1, es, -Ds_y);
+      ws->U[3][t] = fmaf(pa.nR2p1, es, -Ey);
+      ws->U[4][t] = -dvx;
+      ws->U[5][t] = -dax;
+      ws->U[6][t] = -dvy;
+      ws->U[7][t] = -day;
     }
     if (valid) {
       if (RES) res += fmaf((float)n, base, rc) + ec * ec + es * es;
       const float dth = ws->th[t] - psi;
       rps = fmaf(dth, dth, rps);
+    }
+  }
+  __syncwarp();
+  // D2: h partial over this warp's samples (the basis is zero for t >= q)
+  float acc[48];
+#pragma unroll
+  for (int k = 0; k < 48; ++k) acc[k] = 0.f;
+#pragma unroll 1
+  for (int u = w; u < pa.rounds; u += T) {
+    const int t = 32 * u + lane;
+    const float u0 = ws->U[0][t], u1 = ws->U[1][t], u2 = ws->U[2][t], u3 = ws->U[3][t];
+    const float u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const float p = Pt[k * QP + t], pd = Pt[(NV + k) * QP + t], pdd = Pt[(2 * NV + k) * QP + t];
+      acc[k] = fmaf(p, u0, fmaf(pd, u4, fmaf(pdd, u5, acc[k])));
+      acc[NV + k] = fmaf(p, u1, acc[NV + k]);
+      acc[NV2 + k] = fmaf(p, u2, fmaf(pd, u6, fmaf(pdd, u7, acc[NV2 + k])));
+      acc[NV2 + NV + k] = fmaf(p, u3, acc[NV2 + NV + k]);
     }
   }
   const float v32 = transpose_reduce32(acc, lane);
@@ -470,7 +480,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 
 // ---------------------------------------------------------------- kernel
 template <int M>
-__global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ KernelArgs a) {
+__global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
   const int n = a.n, q = a.q, K = a.iters;
@@ -519,6 +529,7 @@ __global__ void __launch_bounds__(256) bmc_am_kernel(const __grid_constant__ Ker
     circ &= (aa == bb);
   }
   for (int i = tid; i < ipc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
+  for (int i = tid; i < ipc * 8 * QP; i += blockDim.x) (&wsbase[i / (8 * QP)].U[0][0])[i % (8 * QP)] = 0.f;
   const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
   __syncthreads();
