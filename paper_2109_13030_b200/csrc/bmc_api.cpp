@@ -240,11 +240,18 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   if (rc != BMC_OK) return rc;
   // launch shape: `team` warps per instance, `ipc` instances per CTA.  One
   // warp per instance by default; BMC_TEAM / BMC_IPC override (experiments).
-  int team = 1, ipc = 4;
+  // Occupancy model: <= 16 warps per SM (<= 128 registers per thread); the
+  // batch is spread so that every SM holds ceil(B / 148) instances, and
+  // small batches spend the spare warps on teams (one 32-sample round each).
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->p.device);
+  const int rounds = (c->q + 31) / 32;
+  int ipc = (int)std::min<int64_t>(16, (pr->B + dev_sms - 1) / dev_sms);
+  int team = std::max(1, std::min(rounds, 16 / std::max(1, ipc)));
   if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
   if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
   if (team < 1 || team > 4) team = 1;
-  if (ipc < 1 || ipc * team > 32) ipc = std::max(1, 4 / team);
+  if (ipc < 1 || ipc * team > 16) ipc = std::max(1, 16 / team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024) --ipc;
   if (kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024)
     return fail(BMC_EINVAL, "n_obs * q too large for shared memory");

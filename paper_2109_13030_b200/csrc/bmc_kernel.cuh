@@ -197,8 +197,8 @@ struct Proj {
 // the MUFU pipe) must run.  In the split tail round lanes of different groups
 // visit different obstacles, so trip counts are made uniform with empty
 // slots.
-template <int M, bool RES, bool SPLIT>
-__device__ __forceinline__ void coll_circ(const float2* __restrict__ ob, const float4* __restrict__ abi,
+template <int M, bool SPLIT>
+__device__ __forceinline__ void coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
                                           int n, int g, int S, const float (&X)[M], const float (&Y)[M],
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                           float (&Dy)[M], float& rc) {
@@ -262,8 +262,9 @@ __device__ __forceinline__ void coll_circ(const float2* __restrict__ ob, const f
 
 // Any obstacle kinds, one obstacle at a time.  GUARD handles x~ = y~ = 0
 // exactly (G18: alpha = 0, d = 1 -> delta = (a, 0)).
-template <int M, bool RES, bool GUARD>
-__device__ __forceinline__ void coll_general(const float2* __restrict__ ob, const float4* __restrict__ abi,
+template <int M>
+__device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, const float2* __restrict__ ob,
+                                             const float4* __restrict__ abi,
                                              int n, int g, int S, const float (&X)[M], const float (&Y)[M],
                                              const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                              float (&Dy)[M], float& rc) {
@@ -311,7 +312,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
   const int nr = (q + 31) >> 5;
 #pragma unroll
   for (int uu = 0; uu < QP / 32; ++uu) {   // unrolled: independent atan2 chains overlap
-    const int u = w + uu * T;                // this warp's rounds within the team
+    const int u = (T - 1 - w) + uu * T;      // this warp's rounds (the leader gets the last, lightest)
     if (u >= nr) break;
     const int t = 32 * u + lane;
     float p[NV];
@@ -341,14 +342,14 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
 //   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
 // written to shared memory; D2: contraction with P, Pdot, Pddot.  Splitting
 // keeps the 44 contraction accumulators out of the obstacle loop's registers.
-template <int M, bool RES>
-__device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws, int lane,
-                                              int w, int T) {
+template <int M>
+__device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, const float (&r)[M], WarpSmem* ws,
+                                              int lane, int w, int T) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
 #pragma unroll 1
-  for (int u = w; u < pa.rounds; u += T) {   // this warp's rounds within the team
+  for (int u = T - 1 - w; u < pa.rounds; u += T) {   // this warp's rounds (leader: the lightest)
     int t, g, S, R;
     if (u < pa.ntf) {
       t = 32 * u + lane; g = 0; S = 1; R = 32;
@@ -399,10 +400,10 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     float rc = 0.f;
     const float2* ob = pa.obs + t;
     if (pa.all_circ) {
-      if (S == 1) coll_circ<M, RES, false>(ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
-      else coll_circ<M, RES, true>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      if (S == 1) coll_circ<M, false>(RES, ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
+      else coll_circ<M, true>(RES, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     } else {
-      coll_general<M, RES, false>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     }
     float chk = rc;
 #pragma unroll
@@ -411,7 +412,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #pragma unroll
       for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
       rc = 0.f;
-      coll_general<M, RES, true>(ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      coll_general<M>(RES, true, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     }
     for (int off = R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
 #pragma unroll
@@ -451,7 +452,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #pragma unroll
   for (int k = 0; k < 48; ++k) acc[k] = 0.f;
 #pragma unroll 1
-  for (int u = w; u < pa.rounds; u += T) {
+  for (int u = T - 1 - w; u < pa.rounds; u += T) {
     const int t = 32 * u + lane;
     const float u0 = ws->U[0][t], u1 = ws->U[1][t], u2 = ws->U[2][t], u3 = ws->U[3][t];
     const float u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
@@ -670,8 +671,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
       team_sync(team, T);
       // ---- D: projections + contraction ---------------------------------------
       const bool want_res = trace ? (it >= 0) : (it == K - 1);
-      if (want_res) phase_project<M, true>(pa, r, ws, lane, w, T);
-      else phase_project<M, false>(pa, r, ws, lane, w, T);
+      phase_project<M>(want_res, pa, r, ws, lane, w, T);
       team_sync(team, T);
       if (lead) {
         for (int kk = lane; kk < 48; kk += 32) {
