@@ -59,7 +59,9 @@ def check(cfg, pr, label, iters=None, lambda_in=None, okw=None, gkw=None, trace=
     gkw = gkw or {}
     g = run_gpu(cfg, pr, iters, lambda_in, trace=trace, **gkw)
     r = run_oracle(cfg, pr, iters, lambda_in, trace=trace, **okw)
-    st = compare(cfg, g, r, cfg.res_tol, label)
+    o = Oracle(oracle_params(cfg, **okw), cfg.n)
+    st = compare(cfg, g, r, cfg.res_tol, label, oracle=o, problem=pr,
+                 iters=cfg.K if iters is None else iters, lambda_in=lambda_in)
     print(st)
     return g, r
 
@@ -98,13 +100,46 @@ def test_c3_full_batch_sampled_instances():
     sub["init"] = pr["init"][idx]
     r = run_oracle(cfg, sub)
     gs = {k: g[k][idx] for k in ("coeffs", "cost", "residual")}
-    compare(cfg, gs, r, cfg.res_tol, "C3 B=1000 sampled", check_best=False)
+    st = compare(cfg, gs, r, cfg.res_tol, "C3 B=1000 sampled", check_best=False,
+                 oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr, idx=idx)
+    print(st)
     # the GPU best must be the argmin key over all instances of its own outputs
     feas = g["residual"][:, 0] <= cfg.res_tol
     assert np.all(np.isfinite(g["cost"]))
     bi = int(g["best"][0])
     if feas.any():
         assert feas[bi] and g["cost"][bi] == g["cost"][feas].min()
+
+
+def test_c4_full_batch_sampled_instances():
+    """C4 (B = 1000, 4 circles, 50 obstacles, tight bounds, K = 200): 12 sampled instances."""
+    cfg = CONFIGS["C4"]
+    pr = make_problem(cfg, 0)
+    g = run_gpu(cfg, pr)
+    idx = np.random.default_rng(7).choice(cfg.B, 12, replace=False)
+    sub = dict(pr)
+    sub["init"] = pr["init"][idx]
+    r = run_oracle(cfg, sub)
+    gs = {k: g[k][idx] for k in ("coeffs", "cost", "residual")}
+    print(compare(cfg, gs, r, cfg.res_tol, "C4 B=1000 sampled", check_best=False,
+                  oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr, idx=idx))
+
+
+def test_large_batch_team_layout_matches_small_batch():
+    """The launch shape depends on B (teams of warps for small batches, one warp per
+    instance for large ones): an instance's result must not depend on it beyond
+    fp32 reassociation of the per-warp partial sums."""
+    cfg = CONFIGS["C3"].with_(K=40)
+    big = make_problem(cfg, 3, B=3000)
+    g_big = run_gpu(cfg, big)
+    small = dict(big)
+    small["init"] = big["init"][:20]
+    g_small = run_gpu(cfg, small)
+    r = run_oracle(cfg, small)
+    for lab, g in (("B=3000 layout", {k: g_big[k][:20] for k in ("coeffs", "cost", "residual")}),
+                   ("B=20 layout", g_small)):
+        compare(cfg, g, r, cfg.res_tol, lab, check_best=False, oracle=Oracle(oracle_params(cfg), cfg.n),
+                problem=small)
 
 
 def test_obstacle_free():
