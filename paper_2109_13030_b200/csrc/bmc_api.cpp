@@ -131,11 +131,9 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
     HostConsts hc;
     std::string err;
     if (build_consts(setup_params(c), 0, &hc, &err) != 0) {
-      delete[] hc.pt;
       delete c;
       return fail(BMC_ESINGULAR, err);
     }
-    delete[] hc.pt;
   }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -183,22 +181,17 @@ static int32_t get_blob(bmc_ctx* c, int n, Blob** out) {
   }
   HostConsts hc;
   std::string err;
-  if (build_consts(setup_params(c), n, &hc, &err) != 0) {
-    delete[] hc.pt;
-    return fail(BMC_ESINGULAR, err);
-  }
+  if (build_consts(setup_params(c), n, &hc, &err) != 0) return fail(BMC_ESINGULAR, err);
   Blob b;
   b.nb = hc.nb;
   const size_t bytes = BlobLayout::bytes(hc.QP);
   cudaError_t e = cudaMalloc(&b.d, bytes);
-  if (e != cudaSuccess) {
-    delete[] hc.pt;
-    return cuda_fail(e, "cudaMalloc(blob)");
-  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(blob)");
   std::vector<unsigned char> host(bytes);
   std::memcpy(host.data(), hc.blob_f64, BlobLayout::bytes_f64);
   std::memcpy(host.data() + BlobLayout::bytes_f64, hc.pt, BlobLayout::bytes_f32(hc.QP));
-  delete[] hc.pt;
+  std::memcpy(host.data() + BlobLayout::bytes_f64 + BlobLayout::bytes_f32(hc.QP), hc.pt64,
+              BlobLayout::bytes_p64(hc.QP));
   e = cudaMemcpy(b.d, host.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(b.d);

@@ -39,7 +39,9 @@ struct BlobLayout {
   static constexpr size_t bytes_f64 = sizeof(double) * n_doubles;
   // fp32 section: Pt[3][11][QP] = P, Pdot, Pddot transposed, zero for t >= q
   BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * 3 * NV * (size_t)QP; }
-  BMC_HD static size_t bytes(int QP) { return bytes_f64 + bytes_f32(QP); }
+  // fp64 copy of the same basis for the F^T (F xi - g) and P^T theta contractions
+  BMC_HD static size_t bytes_p64(int QP) { return sizeof(double) * 3 * NV * (size_t)QP; }
+  BMC_HD static size_t bytes(int QP) { return bytes_f64 + bytes_f32(QP) + bytes_p64(QP); }
 };
 
 // Kernel arguments (passed by value).
@@ -83,7 +85,9 @@ struct SetupParams {
 struct HostConsts {
   int q, QP, nb, n, m;
   double blob_f64[BlobLayout::n_doubles];
-  float* pt = nullptr;   // [3][11][QP]
+  float* pt = nullptr;     // [3][11][QP]
+  double* pt64 = nullptr;  // [3][11][QP]
+  ~HostConsts() { delete[] pt; delete[] pt64; }
 };
 
 // setup.cpp: fp64 constants for obstacle count n; 0 or 2 (singular) with *err.

@@ -53,11 +53,11 @@ struct WarpSmem {
   double xi2[12];
   double rhsp[12];
   float cf[5][12];      // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s, c_psi (padded)
-  float h[48];          // F^T (F xi1 - g), summed over the team's warps
-  float pth[16];        // P^T theta, summed
+  double h[48];         // F^T (F xi1 - g), summed over the team's warps (fp64: it cancels)
+  double pth[16];       // P^T theta, summed
   float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
-  float part_h[T_MAX][48];      // per-warp partials, summed in warp order (deterministic)
-  float part_th[T_MAX][16];
+  double part_h[T_MAX][48];     // per-warp partials, summed in warp order (deterministic)
+  double part_th[T_MAX][16];
   float part_res[T_MAX][4];
   float U[8][QP];               // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2)
 };
@@ -133,17 +133,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // One butterfly stage of the transpose-reduce: CNT values -> CNT/2 values.
-template <int CNT>
-__device__ __forceinline__ void tr_stage(float* v, int off, bool upper) {
+template <int CNT, typename V>
+__device__ __forceinline__ void tr_stage(V* v, int off, bool upper) {
 #pragma unroll
   for (int i = 0; i < CNT / 2; ++i) {
-    const float send = upper ? v[i] : v[i + CNT / 2];
-    const float keep = upper ? v[i + CNT / 2] : v[i];
+    const V send = upper ? v[i] : v[i + CNT / 2];
+    const V keep = upper ? v[i + CNT / 2] : v[i];
     v[i] = keep + __shfl_xor_sync(FULL, send, off);
   }
 }
 // 32 values per lane -> lane l holds the warp total of value l.
-__device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
+template <typename V>
+__device__ __forceinline__ V transpose_reduce32(V* v, int lane) {
   tr_stage<32>(v, 16, lane & 16);
   tr_stage<16>(v, 8, lane & 8);
   tr_stage<8>(v, 4, lane & 4);
@@ -152,7 +153,8 @@ __device__ __forceinline__ float transpose_reduce32(float* v, int lane) {
   return v[0];
 }
 // 16 values per lane -> lane l holds the warp total of value l >> 1.
-__device__ __forceinline__ float transpose_reduce16(float* v, int lane) {
+template <typename V>
+__device__ __forceinline__ V transpose_reduce16(V* v, int lane) {
   tr_stage<16>(v, 16, lane & 16);
   tr_stage<8>(v, 8, lane & 8);
   tr_stage<4>(v, 4, lane & 4);
@@ -172,6 +174,7 @@ __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
 // Per-kernel constants of the projection phase (registers / constant bank).
 struct Proj {
   const float* Pt;       // smem basis [3][11][QP]
+  const double* Pt64;    // the same basis in fp64 (contractions)
   const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
   const float4* abi;     // smem (a, b, a^2 or ab, kind) per obstacle
   int q, n, ntf, rtail, rounds;
@@ -301,14 +304,14 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
-__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSmem* ws, int lane, int q,
-                                            int w, int T) {
+__device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
+                                            WarpSmem* ws, int lane, int q, int w, int T) {
   float cc[NV], cs[NV];
   load12(ws->cf[1], cc);
   load12(ws->cf[3], cs);
-  float acc[16];
+  double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
   const int nr = (q + 31) >> 5;
 #pragma unroll
   for (int uu = 0; uu < QP / 32; ++uu) {   // unrolled: independent atan2 chains overlap
@@ -328,10 +331,11 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, WarpSm
     ws->c[t] = c;
     ws->s[t] = s;
     ws->th[t] = tht;
+    const double thd = (double)tht;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = fmaf(p[k], tht, acc[k]);
+    for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP + t], thd, acc[k]);
   }
-  const float v = transpose_reduce16(acc, lane);
+  const double v = transpose_reduce16(acc, lane);
   if (!(lane & 1) && (lane >> 1) < NV) ws->part_th[w][lane >> 1] = v;
 }
 
@@ -447,26 +451,30 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     }
   }
   __syncwarp();
-  // D2: h partial over this warp's samples (the basis is zero for t >= q)
-  float acc[48];
+  // D2: h partial over this warp's samples (the basis is zero for t >= q).
+  // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so the
+  // sum over samples cancels and fp32 accumulation would dominate the error
+  // (DESIGN.md "Numerics").
+  const double* __restrict__ Pt64 = pa.Pt64;
+  double acc[48];
 #pragma unroll
-  for (int k = 0; k < 48; ++k) acc[k] = 0.f;
+  for (int k = 0; k < 48; ++k) acc[k] = 0.0;
 #pragma unroll 1
   for (int u = T - 1 - w; u < pa.rounds; u += T) {
     const int t = 32 * u + lane;
-    const float u0 = ws->U[0][t], u1 = ws->U[1][t], u2 = ws->U[2][t], u3 = ws->U[3][t];
-    const float u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
+    const double u0 = ws->U[0][t], u1 = ws->U[1][t], u2 = ws->U[2][t], u3 = ws->U[3][t];
+    const double u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const float p = Pt[k * QP + t], pd = Pt[(NV + k) * QP + t], pdd = Pt[(2 * NV + k) * QP + t];
-      acc[k] = fmaf(p, u0, fmaf(pd, u4, fmaf(pdd, u5, acc[k])));
-      acc[NV + k] = fmaf(p, u1, acc[NV + k]);
-      acc[NV2 + k] = fmaf(p, u2, fmaf(pd, u6, fmaf(pdd, u7, acc[NV2 + k])));
-      acc[NV2 + NV + k] = fmaf(p, u3, acc[NV2 + NV + k]);
+      const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
+      acc[k] = fma(p, u0, fma(pd, u4, fma(pdd, u5, acc[k])));
+      acc[NV + k] = fma(p, u1, acc[NV + k]);
+      acc[NV2 + k] = fma(p, u2, fma(pd, u6, fma(pdd, u7, acc[NV2 + k])));
+      acc[NV2 + NV + k] = fma(p, u3, acc[NV2 + NV + k]);
     }
   }
-  const float v32 = transpose_reduce32(acc, lane);
-  const float v16 = transpose_reduce16(acc + 32, lane);
+  const double v32 = transpose_reduce32(acc, lane);
+  const double v16 = transpose_reduce16(acc + 32, lane);
   ws->part_h[w][lane] = v32;
   if (!(lane & 1)) ws->part_h[w][32 + (lane >> 1)] = v16;
   if (RES) {
@@ -487,6 +495,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   const int n = a.n, q = a.q, K = a.iters;
   const double* sf = reinterpret_cast<const double*>(smem);
   const float* Pt = reinterpret_cast<const float*>(smem + BlobLayout::bytes_f64);
+  const double* Pt64 = reinterpret_cast<const double*>(smem + BlobLayout::bytes_f64 + BlobLayout::bytes_f32(QP));
   float2* obs = reinterpret_cast<float2*>(smem + BlobLayout::bytes(QP));
   const int npad = pad_obstacles(n);
   float4* abi = reinterpret_cast<float4*>(obs + (size_t)npad * QP);
@@ -552,6 +561,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
 
   Proj pa;
   pa.Pt = Pt;
+  pa.Pt64 = Pt64;
   pa.obs = obs;
   pa.abi = abi;
   pa.q = q;
@@ -638,11 +648,11 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
       }
       team_sync(team, T);
       // ---- B: heading target ------------------------------------------------
-      phase_theta(Pt, ws, lane, q, w, T);
+      phase_theta(Pt, Pt64, ws, lane, q, w, T);
       team_sync(team, T);
       if (lead) {
       if (k < NV) {
-        float s = 0.f;
+        double s = 0.0;
         for (int ww = 0; ww < T; ++ww) s += ws->part_th[ww][k];
         ws->pth[k] = s;
       }
@@ -675,7 +685,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
       team_sync(team, T);
       if (lead) {
         for (int kk = lane; kk < 48; kk += 32) {
-          float s = 0.f;
+          double s = 0.0;
           for (int ww = 0; ww < T; ++ww) s += ws->part_h[ww][kk];
           ws->h[kk] = s;
         }

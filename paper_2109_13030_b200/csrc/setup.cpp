@@ -189,13 +189,18 @@ int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err)
     for (int rr = 0; rr < nb; ++rr) f[BlobLayout::Kp12t + rr * NV + k] = Kpi[k * Np + NV + rr];
   }
   delete[] out->pt;
+  delete[] out->pt64;
   out->pt = new float[3 * NV * QP];
+  out->pt64 = new double[3 * NV * QP];
   std::memset(out->pt, 0, sizeof(float) * 3 * NV * QP);
+  std::memset(out->pt64, 0, sizeof(double) * 3 * NV * QP);
   for (int k = 0; k < NV; ++k)
     for (int t = 0; t < q; ++t) {
-      out->pt[(0 * NV + k) * QP + t] = (float)P[t * NV + k];
-      out->pt[(1 * NV + k) * QP + t] = (float)Pd[t * NV + k];
-      out->pt[(2 * NV + k) * QP + t] = (float)Pdd[t * NV + k];
+      const double v[3] = {P[t * NV + k], Pd[t * NV + k], Pdd[t * NV + k]};
+      for (int b = 0; b < 3; ++b) {
+        out->pt[(b * NV + k) * QP + t] = (float)v[b];
+        out->pt64[(b * NV + k) * QP + t] = v[b];
+      }
     }
   return 0;
 }
