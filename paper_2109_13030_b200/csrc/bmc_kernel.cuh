@@ -455,28 +455,43 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so the
   // sum over samples cancels and fp32 accumulation would dominate the error
   // (DESIGN.md "Numerics").
+  // Two passes keep 22 (+10 pad) fp64 accumulators live: the position blocks
+  // (P, Pdot, Pddot) of both channels, then the copy blocks (P only).
   const double* __restrict__ Pt64 = pa.Pt64;
-  double acc[48];
-#pragma unroll
-  for (int k = 0; k < 48; ++k) acc[k] = 0.0;
 #pragma unroll 1
-  for (int u = T - 1 - w; u < pa.rounds; u += T) {
-    const int t = 32 * u + lane;
-    const double u0 = ws->U[0][t], u1 = ws->U[1][t], u2 = ws->U[2][t], u3 = ws->U[3][t];
-    const double u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
+  for (int pass = 0; pass < 2; ++pass) {
+    double acc[32];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
-      acc[k] = fma(p, u0, fma(pd, u4, fma(pdd, u5, acc[k])));
-      acc[NV + k] = fma(p, u1, acc[NV + k]);
-      acc[NV2 + k] = fma(p, u2, fma(pd, u6, fma(pdd, u7, acc[NV2 + k])));
-      acc[NV2 + NV + k] = fma(p, u3, acc[NV2 + NV + k]);
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+#pragma unroll 1
+    for (int u = T - 1 - w; u < pa.rounds; u += T) {
+      const int t = 32 * u + lane;
+      if (pass == 0) {
+        const double u0 = ws->U[0][t], u2 = ws->U[2][t];
+        const double u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
+          acc[k] = fma(p, u0, fma(pd, u4, fma(pdd, u5, acc[k])));
+          acc[NV + k] = fma(p, u2, fma(pd, u6, fma(pdd, u7, acc[NV + k])));
+        }
+      } else {
+        const double u1 = ws->U[1][t], u3 = ws->U[3][t];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          const double p = Pt64[k * QP + t];
+          acc[k] = fma(p, u1, acc[k]);
+          acc[NV + k] = fma(p, u3, acc[NV + k]);
+        }
+      }
+    }
+    const double v = transpose_reduce32(acc, lane);   // lane k < 22: output k of this pass
+    if (lane < NV2) {
+      // h layout [ch * 22 + blk * 11 + k]: pass 0 fills blk 0, pass 1 blk 1
+      const int ch = lane / NV, k = lane - ch * NV;
+      ws->part_h[w][ch * NV2 + pass * NV + k] = v;
     }
   }
-  const double v32 = transpose_reduce32(acc, lane);
-  const double v16 = transpose_reduce16(acc + 32, lane);
-  ws->part_h[w][lane] = v32;
-  if (!(lane & 1)) ws->part_h[w][32 + (lane >> 1)] = v16;
   if (RES) {
     res = warp_sum(res);
     rps = warp_sum(rps);
