@@ -348,7 +348,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // keeps the 44 contraction accumulators out of the obstacle loop's registers.
 template <int M>
 __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, const float (&r)[M], WarpSmem* ws,
-                                              int lane, int w, int T) {
+                                              int lane, int w, int T, int team) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
@@ -455,41 +455,35 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so the
   // sum over samples cancels and fp32 accumulation would dominate the error
   // (DESIGN.md "Numerics").
-  // Two passes keep 22 (+10 pad) fp64 accumulators live: the position blocks
-  // (P, Pdot, Pddot) of both channels, then the copy blocks (P only).
+  // The contraction is split by channel: one warp per channel (T = 1: both
+  // in turn; T = 4: two warps per channel over alternate rounds), so each
+  // warp keeps 22 (+10 pad) fp64 accumulators and reduces them once.
+  team_sync(team, T);   // D2 reads every warp's U
   const double* __restrict__ Pt64 = pa.Pt64;
+  const int nch = (T == 1) ? 2 : 1, r0 = (T <= 2) ? 0 : (w >> 1), rstep = (T <= 2) ? 1 : 2;
 #pragma unroll 1
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int ci = 0; ci < nch; ++ci) {
+    const int ch = (T == 1) ? ci : (w & 1);
     double acc[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc[k] = 0.0;
 #pragma unroll 1
-    for (int u = T - 1 - w; u < pa.rounds; u += T) {
+    for (int u = r0; u < pa.rounds; u += rstep) {
       const int t = 32 * u + lane;
-      if (pass == 0) {
-        const double u0 = ws->U[0][t], u2 = ws->U[2][t];
-        const double u4 = ws->U[4][t], u5 = ws->U[5][t], u6 = ws->U[6][t], u7 = ws->U[7][t];
+      // channel x: U0 (P), U1 (copy, P), U4 (Pdot), U5 (Pddot); channel y: U2, U3, U6, U7
+      const double ua = ws->U[2 * ch][t], ub = ws->U[2 * ch + 1][t];
+      const double uv = ws->U[4 + 2 * ch][t], uac = ws->U[5 + 2 * ch][t];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
-          acc[k] = fma(p, u0, fma(pd, u4, fma(pdd, u5, acc[k])));
-          acc[NV + k] = fma(p, u2, fma(pd, u6, fma(pdd, u7, acc[NV + k])));
-        }
-      } else {
-        const double u1 = ws->U[1][t], u3 = ws->U[3][t];
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          const double p = Pt64[k * QP + t];
-          acc[k] = fma(p, u1, acc[k]);
-          acc[NV + k] = fma(p, u3, acc[NV + k]);
-        }
+      for (int k = 0; k < NV; ++k) {
+        const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
+        acc[k] = fma(p, ua, fma(pd, uv, fma(pdd, uac, acc[k])));
+        acc[NV + k] = fma(p, ub, acc[NV + k]);
       }
     }
-    const double v = transpose_reduce32(acc, lane);   // lane k < 22: output k of this pass
+    const double v = transpose_reduce32(acc, lane);   // lane k < 22: entry k of channel ch
     if (lane < NV2) {
-      // h layout [ch * 22 + blk * 11 + k]: pass 0 fills blk 0, pass 1 blk 1
-      const int ch = lane / NV, k = lane - ch * NV;
-      ws->part_h[w][ch * NV2 + pass * NV + k] = v;
+      ws->part_h[w][ch * NV2 + lane] = v;
+      if (T > 1) ws->part_h[w][(1 - ch) * NV2 + lane] = 0.0;
     }
   }
   if (RES) {
@@ -696,7 +690,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
       team_sync(team, T);
       // ---- D: projections + contraction ---------------------------------------
       const bool want_res = trace ? (it >= 0) : (it == K - 1);
-      phase_project<M>(want_res, pa, r, ws, lane, w, T);
+      phase_project<M>(want_res, pa, r, ws, lane, w, T, team);
       team_sync(team, T);
       if (lead) {
         for (int kk = lane; kk < 48; kk += 32) {
