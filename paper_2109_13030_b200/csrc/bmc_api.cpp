@@ -244,6 +244,7 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
   if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
   if (team < 1 || team > 4) team = 1;
+  if (team == 3) team = (ipc * 4 <= 16) ? 4 : 2;   // the D2 channel split needs T in {1, 2, 4}
   if (ipc < 1 || ipc * team > 16) ipc = std::max(1, 16 / team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024) --ipc;
   if (kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024)
