@@ -180,6 +180,7 @@ struct Proj {
   int q, n, ntf, rtail, rounds;
   bool all_circ;
   float nR1, nR2p1, v_max, a_max, vref_x, vref_y;
+  float rlo, rhi;        // extent of the circle offsets along the heading
 };
 
 // --------------------------------------------------- collision projections
@@ -200,9 +201,17 @@ struct Proj {
 // the MUFU pipe) must run.  In the split tail round lanes of different groups
 // visit different obstacles, so trip counts are made uniform with empty
 // slots.
+//
+// The first pass tests the segment of circle centres {x + r u : r in
+// [rlo, rhi]}, u = (cos psi, sin psi), instead of each centre: with
+// d = x - o, min_r |d + r u|^2 = D0 + 2 r* B + r*^2, D0 = |d|^2, B = d.u,
+// r* = clamp(-B, rlo, rhi) -- a lower bound of every centre's distance, so the
+// test is conservative (exact cases only ever go to the second pass) and
+// costs the same for any number of circles.
 template <int M, bool SPLIT>
 __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
                                           int n, int g, int S, const float (&X)[M], const float (&Y)[M],
+                                          float xc, float yc, float cu, float su, float rlo, float rhi,
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                           float (&Dy)[M], float& rc) {
   const int trips = SPLIT ? (n + S - 1) / S : pad_obstacles(n);
@@ -223,14 +232,12 @@ __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restri
           const int jcl = have ? j : 0;
           const float2 o = ob[jcl * QP];
           const float a2 = abi[jcl].z;
-          float rmin = 0.f;
-#pragma unroll
-          for (int i = 0; i < M; ++i) {
-            const float xt = X[i] - o.x, yt = Y[i] - o.y;
-            const float r2 = fmaf(yt, yt, xt * xt);
-            rmin = (i == 0) ? r2 : fminf(rmin, r2);
-          }
-          mask[bk] |= (have && rmin < a2) ? (1u << jj) : 0u;
+          const float dx = xc - o.x, dy = yc - o.y;
+          const float d0 = fmaf(dy, dy, dx * dx), bd = fmaf(dy, su, dx * cu);
+          const float rs = fmaxf(rlo, fminf(rhi, -bd));
+          const float qmin = fmaf(rs, fmaf(2.f, bd, rs), d0);
+          // margin: absolute rounding of qmin is < 1e-6 m^2 for any obstacle within reach
+          mask[bk] |= (have && qmin < fmaf(a2, 1.00001f, 1e-5f)) ? (1u << jj) : 0u;
         }
       }
     }
@@ -404,8 +411,10 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     float rc = 0.f;
     const float2* ob = pa.obs + t;
     if (pa.all_circ) {
-      if (S == 1) coll_circ<M, false>(RES, ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
-      else coll_circ<M, true>(RES, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      if (S == 1)
+        coll_circ<M, false>(RES, ob, pa.abi, n, 0, 1, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s, Dx, Dy, rc);
+      else
+        coll_circ<M, true>(RES, ob, pa.abi, n, g, S, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s, Dx, Dy, rc);
     } else {
       coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     }
@@ -590,6 +599,12 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   pa.a_max = a.a_max;
   pa.vref_x = (float)(a.ref_dx / a.T);
   pa.vref_y = (float)(a.ref_dy / a.T);
+  pa.rlo = a.r[0];
+  pa.rhi = a.r[0];
+  for (int i = 1; i < M; ++i) {
+    pa.rlo = fminf(pa.rlo, a.r[i]);
+    pa.rhi = fmaxf(pa.rhi, a.r[i]);
+  }
   float r[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
