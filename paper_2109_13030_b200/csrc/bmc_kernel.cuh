@@ -162,6 +162,25 @@ __device__ __forceinline__ V transpose_reduce16(V* v, int lane) {
   return v[0] + __shfl_xor_sync(FULL, v[0], 1);
 }
 
+// N (power of two <= 32) values per lane -> after log2 N transpose stages each
+// lane holds a partial of value lane >> (5 - log2 N); plain butterflies over
+// the remaining lane bits finish the warp total.
+template <int CNT, int OFF, typename V>
+__device__ __forceinline__ void tr_stages(V* v, int lane) {
+  if constexpr (CNT > 1) {
+    tr_stage<CNT>(v, OFF, lane & OFF);
+    tr_stages<CNT / 2, OFF / 2>(v, lane);
+  }
+}
+template <int N, typename V>
+__device__ __forceinline__ V tr_reduce(V* v, int lane) {
+  tr_stages<N, 16>(v, lane);
+  constexpr int first_plain = 16 / N;   // offset after the transpose stages
+#pragma unroll
+  for (int o = first_plain; o >= 1; o >>= 1) v[0] += __shfl_xor_sync(FULL, v[0], o);
+  return v[0];
+}
+
 __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
   const float4 a = reinterpret_cast<const float4*>(src)[0];
   const float4 b = reinterpret_cast<const float4*>(src)[1];
@@ -215,7 +234,7 @@ __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restri
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                           float (&Dy)[M], float& rc) {
   const int trips = SPLIT ? (n + S - 1) / S : pad_obstacles(n);
-  constexpr int NBK = 4;   // blocks per chunk: their REDUX.OR votes are issued back to back
+  constexpr int NBK = 1;   // blocks per chunk (kept at 1: the hot loop must stay in the I-cache)
 #pragma unroll 1
   for (int jc0 = 0; jc0 < trips; jc0 += NBK * JB) {
     unsigned mask[NBK];
@@ -320,8 +339,8 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
   const int nr = (q + 31) >> 5;
-#pragma unroll
-  for (int uu = 0; uu < QP / 32; ++uu) {   // unrolled: independent atan2 chains overlap
+#pragma unroll 1
+  for (int uu = 0; uu < QP / 32; ++uu) {
     const int u = (T - 1 - w) + uu * T;      // this warp's rounds (the leader gets the last, lightest)
     if (u >= nr) break;
     const int t = 32 * u + lane;
@@ -342,8 +361,11 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP + t], thd, acc[k]);
   }
-  const double v = transpose_reduce16(acc, lane);
-  if (!(lane & 1) && (lane >> 1) < NV) ws->part_th[w][lane >> 1] = v;
+  // 11 entries as 8 + 4 transpose-reduce slots
+  const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
+  const double v4 = tr_reduce<4>(acc + 8, lane);    // entry 8 + (lane >> 3)
+  if (!(lane & 3)) ws->part_th[w][lane >> 2] = v8;
+  if (!(lane & 7) && 8 + (lane >> 3) < NV) ws->part_th[w][8 + (lane >> 3)] = v4;
 }
 
 // ---------------------------------------------------------------- phase D
@@ -413,8 +435,8 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     if (pa.all_circ) {
       if (S == 1)
         coll_circ<M, false>(RES, ob, pa.abi, n, 0, 1, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s, Dx, Dy, rc);
-      else
-        coll_circ<M, true>(RES, ob, pa.abi, n, g, S, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s, Dx, Dy, rc);
+      else   // split tail round: few obstacles per lane, the plain loop is smaller code
+        coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     } else {
       coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
     }
@@ -473,9 +495,9 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
 #pragma unroll 1
   for (int ci = 0; ci < nch; ++ci) {
     const int ch = (T == 1) ? ci : (w & 1);
-    double acc[32];
+    double acc[24];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    for (int k = 0; k < 24; ++k) acc[k] = 0.0;
 #pragma unroll 1
     for (int u = r0; u < pa.rounds; u += rstep) {
       const int t = 32 * u + lane;
@@ -489,11 +511,12 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
         acc[NV + k] = fma(p, ub, acc[NV + k]);
       }
     }
-    const double v = transpose_reduce32(acc, lane);   // lane k < 22: entry k of channel ch
-    if (lane < NV2) {
-      ws->part_h[w][ch * NV2 + lane] = v;
-      if (T > 1) ws->part_h[w][(1 - ch) * NV2 + lane] = 0.0;
-    }
+    // 22 entries as 16 + 8 transpose-reduce slots (22 + 3 butterflies, not 31)
+    const double v16 = tr_reduce<16>(acc, lane);       // entry lane >> 1
+    const double v8 = tr_reduce<8>(acc + 16, lane);    // entry 16 + (lane >> 2)
+    if (!(lane & 1)) ws->part_h[w][ch * NV2 + (lane >> 1)] = v16;
+    if (!(lane & 3) && 16 + (lane >> 2) < NV2) ws->part_h[w][ch * NV2 + 16 + (lane >> 2)] = v8;
+    if (T > 1 && lane < NV2) ws->part_h[w][(1 - ch) * NV2 + lane] = 0.0;
   }
   if (RES) {
     res = warp_sum(res);
@@ -611,8 +634,13 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
 
   WarpSmem* ws = wsbase + team;
   const bool lead = (w == 0);   // the team leader owns the fp64 state and the dense steps
-  const long long l = (long long)blockIdx.x * ipc + team;
-  if (l < a.B && team < ipc) {
+  // Every warp runs the iteration (a warp past the end of the batch redoes the
+  // last instance and writes nothing): no branch around the shuffles, so the
+  // compiler emits no divergence fallback paths for them.
+  const long long l_raw = (long long)blockIdx.x * ipc + team;
+  const bool active = l_raw < a.B;
+  const long long l = active ? l_raw : a.B - 1;
+  {
     const int k = lane;
     const double rho = a.rho, rho_psi = a.rho_psi;
     // Bernstein control points of the boundary line (linear precision: c_k = x0 + dx k / 10)
@@ -728,11 +756,11 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
             lamX -= rho * (double)ws->h[k];
             lamY -= rho * (double)ws->h[NV2 + k];
           }
-          if (trace && lane == 0) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
+          if (trace && lane == 0 && active) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
         }
       }
     }
-    if (lead) {
+    if (lead && active) {
 
     // ---- outputs ------------------------------------------------------------
     double jpart = 0.0;
