@@ -46,18 +46,20 @@ constexpr int JB = 8;       // obstacles per inside-test block
 
 constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per round
 
-// Per-instance state shared by the T warps of its team.
+// Per-instance state shared by the T warps of its team.  The x and y channels
+// of xi1 are decoupled in the xi1 step and the lambda step (Eq. 10: F and the
+// KKT are block diagonal over channels), so a team gives each channel to one
+// warp; the small heading step runs redundantly in every warp.
 struct WarpSmem {
-  double xi1[2 * NV2];  // [k][ch]
-  double rhs[2 * NV2];  // [k][ch]
-  double xi2[12];
-  double rhsp[12];
-  float cf[5][12];      // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s, c_psi (padded)
-  double h[48];         // F^T (F xi1 - g), summed over the team's warps (fp64: it cancels)
-  double pth[16];       // P^T theta, summed
+  double xi1[2][24];      // [ch][k] current xi1 (fp64), written by the channel's owner
+  double rhs[2][24];      // [ch][k] lambda - rho h
+  double h[2][24];        // [ch][k] F^T (F xi1 - g) (fp64: it cancels), owner-written
+  double xi2w[T_MAX][12]; // per-warp copies of xi2 (the heading step is redundant)
+  double rhspw[T_MAX][12];
+  float cf[4][12];        // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s (padded)
+  float cf4[T_MAX][12];   // per-warp fp32 c_psi
   float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
-  double part_h[T_MAX][48];     // per-warp partials, summed in warp order (deterministic)
-  double part_th[T_MAX][16];
+  double part_th[T_MAX][16];    // per-warp P^T theta partials, summed in warp order
   float part_res[T_MAX][4];
   float U[8][QP];               // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2)
 };
@@ -397,7 +399,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       float cx[NV], cy[NV], cp[NV];
       load12(ws->cf[0], cx);
       load12(ws->cf[2], cy);
-      load12(ws->cf[4], cp);
+      load12(ws->cf4[w], cp);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const float p = Pt[k * QP + t], pd = Pt[(NV + k) * QP + t], pdd = Pt[(2 * NV + k) * QP + t];
@@ -491,15 +493,17 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   // warp keeps 22 (+10 pad) fp64 accumulators and reduces them once.
   team_sync(team, T);   // D2 reads every warp's U
   const double* __restrict__ Pt64 = pa.Pt64;
-  const int nch = (T == 1) ? 2 : 1, r0 = (T <= 2) ? 0 : (w >> 1), rstep = (T <= 2) ? 1 : 2;
+  // channel owners (T = 1: the warp owns both; T >= 2: warps 0 and 1) contract
+  // their channel over every round
+  const int nch = (T == 1) ? 2 : (w < 2 ? 1 : 0);
 #pragma unroll 1
   for (int ci = 0; ci < nch; ++ci) {
-    const int ch = (T == 1) ? ci : (w & 1);
+    const int ch = (T == 1) ? ci : w;
     double acc[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) acc[k] = 0.0;
 #pragma unroll 1
-    for (int u = r0; u < pa.rounds; u += rstep) {
+    for (int u = 0; u < pa.rounds; ++u) {
       const int t = 32 * u + lane;
       // channel x: U0 (P), U1 (copy, P), U4 (Pdot), U5 (Pddot); channel y: U2, U3, U6, U7
       const double ua = ws->U[2 * ch][t], ub = ws->U[2 * ch + 1][t];
@@ -514,9 +518,8 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     // 22 entries as 16 + 8 transpose-reduce slots (22 + 3 butterflies, not 31)
     const double v16 = tr_reduce<16>(acc, lane);       // entry lane >> 1
     const double v8 = tr_reduce<8>(acc + 16, lane);    // entry 16 + (lane >> 2)
-    if (!(lane & 1)) ws->part_h[w][ch * NV2 + (lane >> 1)] = v16;
-    if (!(lane & 3) && 16 + (lane >> 2) < NV2) ws->part_h[w][ch * NV2 + 16 + (lane >> 2)] = v8;
-    if (T > 1 && lane < NV2) ws->part_h[w][(1 - ch) * NV2 + lane] = 0.0;
+    if (!(lane & 1)) ws->h[ch][lane >> 1] = v16;
+    if (!(lane & 3) && 16 + (lane >> 2) < NV2) ws->h[ch][16 + (lane >> 2)] = v8;
   }
   if (RES) {
     res = warp_sum(res);
@@ -579,7 +582,9 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
     abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
     circ &= (aa == bb);
   }
-  for (int i = tid; i < ipc * 5 * 12; i += blockDim.x) (&wsbase[i / 60].cf[0][0])[i % 60] = 0.f;
+  for (int i = tid; i < ipc * 4 * 12; i += blockDim.x) (&wsbase[i / 48].cf[0][0])[i % 48] = 0.f;
+  for (int i = tid; i < ipc * T_MAX * 12; i += blockDim.x)
+    (&wsbase[i / (T_MAX * 12)].cf4[0][0])[i % (T_MAX * 12)] = 0.f;
   for (int i = tid; i < ipc * 8 * QP; i += blockDim.x) (&wsbase[i / (8 * QP)].U[0][0])[i % (8 * QP)] = 0.f;
   const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
@@ -633,7 +638,6 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
 
   WarpSmem* ws = wsbase + team;
-  const bool lead = (w == 0);   // the team leader owns the fp64 state and the dense steps
   // Every warp runs the iteration (a warp past the end of the batch redoes the
   // last instance and writes nothing): no branch around the shuffles, so the
   // compiler emits no divergence fallback paths for them.
@@ -643,168 +647,168 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   {
     const int k = lane;
     const double rho = a.rho, rho_psi = a.rho_psi;
-    // Bernstein control points of the boundary line (linear precision: c_k = x0 + dx k / 10)
-    const double crefx = (k < NV) ? fma(a.ref_dx, (double)k / (NV - 1), a.ref_x0) : 0.0;
-    const double crefy = (k < NV) ? fma(a.ref_dy, (double)k / (NV - 1), a.ref_y0) : 0.0;
-    double xiX = 0.0, xiY = 0.0, lamX = 0.0, lamY = 0.0, xi2r = 0.0, lamp = 0.0;
+    // channels owned by this warp (phases A, D2, E): both for T = 1, channel w for w < 2
+    const int nown = (T == 1) ? 2 : (w < 2 ? 1 : 0);
+    const int chb = (T == 1) ? 0 : w;
+    double xi[2] = {0.0, 0.0}, lam[2] = {0.0, 0.0}, cref[2] = {0.0, 0.0};
     const float* ini = a.init + l * 3 * NV;
-    if (k < NV) {   // step 1: xi2 from the input, copies start at 0 (G15)
-      xiX = ini[k];
-      xiY = ini[NV + k];
-      xi2r = ini[2 * NV + k];
+    const float* li = a.lambda_in ? a.lambda_in + l * 5 * NV : nullptr;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (c >= nown) break;
+      const int ch = chb + c;
+      // Bernstein control points of the boundary line (linear precision: c_k = x0 + dx k / 10)
+      const double r0 = ch ? a.ref_y0 : a.ref_x0, rd = ch ? a.ref_dy : a.ref_dx;
+      cref[c] = (k < NV) ? fma(rd, (double)k / (NV - 1), r0) : 0.0;
+      if (k < NV) xi[c] = ini[ch * NV + k];   // step 1: copies start at 0 (G15)
+      if (li && k < NV2) lam[c] = li[ch * NV2 + k];
     }
-    if (a.lambda_in) {
-      const float* li = a.lambda_in + l * 5 * NV;
-      if (k < NV2) { lamX = li[k]; lamY = li[NV2 + k]; }
-      if (k < NV) lamp = li[2 * NV2 + k];
-    }
-    if (lead && k < NV) { ws->cf[4][k] = (float)xi2r; ws->xi2[k] = xi2r; }
+    double xi2r = (k < NV) ? (double)ini[2 * NV + k] : 0.0;
+    double lamp = (li && k < NV) ? (double)li[2 * NV2 + k] : 0.0;
+    if (k < NV) { ws->cf4[w][k] = (float)xi2r; ws->xi2w[w][k] = xi2r; }
 
     float r1sq = 0.f, rpsq = 0.f;
     const bool trace = a.res_trace != nullptr;
     // it = -1 is the initialisation of xi3, xi4 / g on the initial trajectory
     // (G15); every phase has a single call site so each is inlined once.
-    // Team protocol per iteration: leader A | all B | leader C | all D | leader E,
-    // separated by team barriers; partial sums are combined in warp order.
+    // Team protocol per iteration: A (channel owners) | B (all, own rounds) |
+    // C (all, redundant) + D1 (all, own rounds) | D2 + E (channel owners).
 #pragma unroll 1
     for (int it = -1; it < K; ++it) {
-      if (lead) {
-      if (it >= 0) {
-        // ---- A: xi1 step ---------------------------------------------------
-        if (k < NV2) {
-          ws->rhs[2 * k] = lamX - rho * (double)ws->h[k];
-          ws->rhs[2 * k + 1] = lamY - rho * (double)ws->h[NV2 + k];
-        }
-        __syncwarp();
-        if (k < NV2) {
-          double ax = ub[k], ay = ub[NV2 + k], bx = 0.0, by = 0.0;
-#pragma unroll 11
-          for (int j = 0; j < NV2; ++j) {
-            const double mkj = sf[BlobLayout::Mt + j * NV2 + k];
-            const double kkj = sf[BlobLayout::K11t + j * NV2 + k];
-            const double2 xj = reinterpret_cast<const double2*>(ws->xi1)[j];
-            const double2 rj = reinterpret_cast<const double2*>(ws->rhs)[j];
-            ax = fma(mkj, xj.x, ax);
-            ay = fma(mkj, xj.y, ay);
-            bx = fma(kkj, rj.x, bx);
-            by = fma(kkj, rj.y, by);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c >= nown) break;
+        const int ch = chb + c;
+        if (it >= 0) {
+          // ---- A: xi1 step, Eq. 13/17 via Eq. 4 (fp64) ---------------------
+          if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * ws->h[ch][k];
+          __syncwarp();
+          if (k < NV2) {
+            double a0 = ub[ch * NV2 + k], a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NV2; j += 2) {
+              a0 = fma(sf[BlobLayout::Mt + j * NV2 + k], ws->xi1[ch][j], a0);
+              a1 = fma(sf[BlobLayout::Mt + (j + 1) * NV2 + k], ws->xi1[ch][j + 1], a1);
+              b0 = fma(sf[BlobLayout::K11t + j * NV2 + k], ws->rhs[ch][j], b0);
+              b1 = fma(sf[BlobLayout::K11t + (j + 1) * NV2 + k], ws->rhs[ch][j + 1], b1);
+            }
+            xi[c] = (a0 + a1) + (b0 + b1);
           }
-          xiX = ax + bx;
-          xiY = ay + by;
+          __syncwarp();
         }
-        __syncwarp();
-      }
-      if (k < NV) { ws->cf[0][k] = (float)(xiX - crefx); ws->cf[2][k] = (float)(xiY - crefy); }
-      else if (k < NV2) { ws->cf[1][k - NV] = (float)xiX; ws->cf[3][k - NV] = (float)xiY; }
-      if (k < NV2) { ws->xi1[2 * k] = xiX; ws->xi1[2 * k + 1] = xiY; }
+        if (k < NV) ws->cf[2 * ch][k] = (float)(xi[c] - cref[c]);
+        else if (k < NV2) ws->cf[2 * ch + 1][k - NV] = (float)xi[c];
+        if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
       team_sync(team, T);
-      // ---- B: heading target ------------------------------------------------
+      // ---- B: heading target --------------------------------------------------
       phase_theta(Pt, Pt64, ws, lane, q, w, T);
       team_sync(team, T);
-      if (lead) {
-      if (k < NV) {
-        double s = 0.0;
-        for (int ww = 0; ww < T; ++ww) s += ws->part_th[ww][k];
-        ws->pth[k] = s;
+      // ---- C: xi2 step + lambda_psi (Eq. 19, 23b), every warp, same order ------
+      double pth = 0.0;
+      if (k < NV)
+        for (int ww = 0; ww < T; ++ww) pth += ws->part_th[ww][k];
+      if (it >= 0) {
+        if (k < NV) ws->rhspw[w][k] = lamp + rho_psi * pth;
+        __syncwarp();
+        if (k < NV) {
+          double s0 = ub[2 * NV2 + k], s1 = 0.0;
+#pragma unroll
+          for (int j = 0; j < NV; j += 2) {
+            s0 = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhspw[w][j], s0);
+            if (j + 1 < NV) s1 = fma(sf[BlobLayout::Kp11t + (j + 1) * NV + k], ws->rhspw[w][j + 1], s1);
+          }
+          xi2r = s0 + s1;
+          ws->xi2w[w][k] = xi2r;
+          ws->cf4[w][k] = (float)xi2r;
+        }
+        __syncwarp();
+        if (k < NV) {
+          double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+          for (int j = 0; j < NV; j += 2) {
+            g0 = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2w[w][j], g0);
+            if (j + 1 < NV) g1 = fma(sf[BlobLayout::Gppt + (j + 1) * NV + k], ws->xi2w[w][j + 1], g1);
+          }
+          lamp -= (g0 + g1) - rho_psi * pth;
+        }
       }
       __syncwarp();
-      if (it >= 0) {
-        // ---- C: xi2 step + lambda_psi ----------------------------------------
-        if (k < NV) ws->rhsp[k] = lamp + rho_psi * (double)ws->pth[k];
-        __syncwarp();
-        if (k < NV) {
-          double s = ub[2 * NV2 + k];
-#pragma unroll
-          for (int j = 0; j < NV; ++j) s = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhsp[j], s);
-          xi2r = s;
-          ws->xi2[k] = s;
-          ws->cf[4][k] = (float)s;
-        }
-        __syncwarp();
-        if (k < NV) {
-          double gs = 0.0;
-#pragma unroll
-          for (int j = 0; j < NV; ++j) gs = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2[j], gs);
-          lamp -= gs - rho_psi * (double)ws->pth[k];
-        }
-      }
-      }
-      team_sync(team, T);
-      // ---- D: projections + contraction ---------------------------------------
+      // ---- D: projections (own rounds) + contraction (owned channels) ---------
       const bool want_res = trace ? (it >= 0) : (it == K - 1);
       phase_project<M>(want_res, pa, r, ws, lane, w, T, team);
-      team_sync(team, T);
-      if (lead) {
-        for (int kk = lane; kk < 48; kk += 32) {
-          double s = 0.0;
-          for (int ww = 0; ww < T; ++ww) s += ws->part_h[ww][kk];
-          ws->h[kk] = s;
-        }
-        if (want_res) {
-          r1sq = 0.f;
-          rpsq = 0.f;
-          for (int ww = 0; ww < T; ++ww) {
-            r1sq += ws->part_res[ww][0];
-            rpsq += ws->part_res[ww][1];
-          }
-        }
-        __syncwarp();
-        if (it >= 0) {
-          // ---- E: multipliers --------------------------------------------------
-          if (k < NV2) {
-            lamX -= rho * (double)ws->h[k];
-            lamY -= rho * (double)ws->h[NV2 + k];
-          }
-          if (trace && lane == 0 && active) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
+      __syncwarp();
+      if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
+        r1sq = 0.f;
+        rpsq = 0.f;
+        for (int ww = 0; ww < T; ++ww) {
+          r1sq += ws->part_res[ww][0];
+          rpsq += ws->part_res[ww][1];
         }
       }
-    }
-    if (lead && active) {
-
-    // ---- outputs ------------------------------------------------------------
-    double jpart = 0.0;
-    if (k < NV) {   // J = sum_ch c^T (Pdd^T Pdd) c, fp64 (Eq. 1a, G17)
-      double gx = 0.0, gy = 0.0, gp = 0.0;
+      if (it >= 0) {
+        // ---- E: multipliers (Eq. 23a with F^T, G3) -------------------------------
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const double gg = sf[BlobLayout::Gdd + j * NV + k];
-        gx = fma(gg, ws->xi1[2 * j], gx);
-        gy = fma(gg, ws->xi1[2 * j + 1], gy);
-        gp = fma(gg, ws->xi2[j], gp);
+        for (int c = 0; c < 2; ++c) {
+          if (c >= nown) break;
+          if (k < NV2) lam[c] -= rho * ws->h[chb + c][k];
+        }
+        if (trace && w == 0 && lane == 0 && active) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
       }
-      jpart = gx * xiX + gy * xiY + gp * xi2r;
     }
-    const double J = warp_sum(jpart);
-    float* co = a.coeffs + l * 5 * NV;
-    if (k < NV2) { co[k] = (float)xiX; co[NV2 + k] = (float)xiY; }
-    if (k < NV) co[2 * NV2 + k] = (float)xi2r;
-    if (a.lambda_out) {
-      float* lo = a.lambda_out + l * 5 * NV;
-      if (k < NV2) { lo[k] = (float)lamX; lo[NV2 + k] = (float)lamY; }
-      if (k < NV) lo[2 * NV2 + k] = (float)lamp;
-    }
-    if (lane == 0) {
-      const float r1 = sqrtf(fmaxf(r1sq, 0.f)), rp = sqrtf(rpsq);
-      a.residual[2 * l] = r1;
-      a.residual[2 * l + 1] = rp;
-      a.cost[l] = (float)J;
-      // packed argmin key (G17): infeasible << 62 | fp32 bits(value) << 30 | index
-      unsigned long long infeasible = !((double)r1 <= a.res_tol);
-      const double v = infeasible ? (double)r1 : J;
-      const float vf = __double2float_rn(v);
-      unsigned bits;
-      if (!isfinite(v) || !isfinite(vf) || !isfinite(J) || !isfinite(r1)) {
-        infeasible = 1;
-        bits = 0x7F800000u;
-      } else {
-        bits = __float_as_uint(vf > 0.f ? vf : 0.f);
+    // ---- outputs ----------------------------------------------------------------
+    if (active) {
+      float* co = a.coeffs + l * 5 * NV;
+      float* lo = a.lambda_out ? a.lambda_out + l * 5 * NV : nullptr;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c >= nown) break;
+        const int ch = chb + c;
+        if (k < NV2) {
+          co[ch * NV2 + k] = (float)xi[c];
+          if (lo) lo[ch * NV2 + k] = (float)lam[c];
+        }
       }
-      const unsigned long long gidx = (unsigned long long)(a.index_base + l) & ((1ull << 30) - 1);
-      const unsigned long long key = (infeasible << 62) | ((unsigned long long)bits << 30) | gidx;
-      atomicMin(a.ws_key, key);
-      __threadfence();
-    }
+      if (w == 0) {
+        if (k < NV) {
+          co[2 * NV2 + k] = (float)xi2r;
+          if (lo) lo[2 * NV2 + k] = (float)lamp;
+        }
+        double jpart = 0.0;
+        if (k < NV) {   // J = sum_ch c^T (Pdd^T Pdd) c, fp64 (Eq. 1a, G17)
+          double gx = 0.0, gy = 0.0, gp = 0.0;
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            const double gg = sf[BlobLayout::Gdd + j * NV + k];
+            gx = fma(gg, ws->xi1[0][j], gx);
+            gy = fma(gg, ws->xi1[1][j], gy);
+            gp = fma(gg, ws->xi2w[0][j], gp);
+          }
+          jpart = gx * ws->xi1[0][k] + gy * ws->xi1[1][k] + gp * xi2r;
+        }
+        const double J = warp_sum(jpart);
+        if (lane == 0) {
+          const float r1 = sqrtf(fmaxf(r1sq, 0.f)), rp = sqrtf(rpsq);
+          a.residual[2 * l] = r1;
+          a.residual[2 * l + 1] = rp;
+          a.cost[l] = (float)J;
+          // packed argmin key (G17): infeasible << 62 | fp32 bits(value) << 30 | index
+          unsigned long long infeasible = !((double)r1 <= a.res_tol);
+          const double v = infeasible ? (double)r1 : J;
+          const float vf = __double2float_rn(v);
+          unsigned bits;
+          if (!isfinite(v) || !isfinite(vf) || !isfinite(J) || !isfinite(r1)) {
+            infeasible = 1;
+            bits = 0x7F800000u;
+          } else {
+            bits = __float_as_uint(vf > 0.f ? vf : 0.f);
+          }
+          const unsigned long long gidx = (unsigned long long)(a.index_base + l) & ((1ull << 30) - 1);
+          const unsigned long long key = (infeasible << 62) | ((unsigned long long)bits << 30) | gidx;
+          atomicMin(a.ws_key, key);
+          __threadfence();
+        }
+      }
     }
   }
   // ---- grid-wide argmin: the last CTA publishes and resets the workspace ----
