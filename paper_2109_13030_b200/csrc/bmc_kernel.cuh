@@ -488,9 +488,16 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so the
   // sum over samples cancels and fp32 accumulation would dominate the error
   // (DESIGN.md "Numerics").
-  // The contraction is split by channel: one warp per channel (T = 1: both
-  // in turn; T = 4: two warps per channel over alternate rounds), so each
-  // warp keeps 22 (+10 pad) fp64 accumulators and reduces them once.
+  if (RES) {   // residual partials must be visible to the team before the barrier
+    res = warp_sum(res);
+    rps = warp_sum(rps);
+    if (lane == 0) {
+      ws->part_res[w][0] = res;
+      ws->part_res[w][1] = rps;
+    }
+  }
+  // The contraction is split by channel (T = 1: the warp does both in turn;
+  // T >= 2: warps 0 and 1 own x and y), 22 fp64 accumulators per lane.
   team_sync(team, T);   // D2 reads every warp's U
   const double* __restrict__ Pt64 = pa.Pt64;
   // channel owners (T = 1: the warp owns both; T >= 2: warps 0 and 1) contract
@@ -520,14 +527,6 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     const double v8 = tr_reduce<8>(acc + 16, lane);    // entry 16 + (lane >> 2)
     if (!(lane & 1)) ws->h[ch][lane >> 1] = v16;
     if (!(lane & 3) && 16 + (lane >> 2) < NV2) ws->h[ch][16 + (lane >> 2)] = v8;
-  }
-  if (RES) {
-    res = warp_sum(res);
-    rps = warp_sum(rps);
-    if (lane == 0) {
-      ws->part_res[w][0] = res;
-      ws->part_res[w][1] = rps;
-    }
   }
 }
 
