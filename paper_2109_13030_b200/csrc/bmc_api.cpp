@@ -303,9 +303,30 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   a.ref_y0 = has0 ? pr->bnd[1][0] : (hasT ? pr->bnd[1][3] : 0.0);
   a.ref_dx = (has0 && hasT) ? pr->bnd[0][3] - pr->bnd[0][0] : 0.0;
   a.ref_dy = (has0 && hasT) ? pr->bnd[1][3] - pr->bnd[1][0] : 0.0;
+  // development aid: BMC_PROF=1 with a PROFILE=1 build prints per-phase cycles
+  const bool prof = std::getenv("BMC_PROF") != nullptr;
+  const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
+  if (prof && cudaMalloc(&a.prof, sizeof(long long) * 10 * nwarps) == cudaSuccess)
+    cudaMemsetAsync(a.prof, 0, sizeof(long long) * 10 * nwarps, s);
   cudaError_t e = launch_am(a, wpc, s);
   c->last_launches = 1;
   if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");
+  if (prof && a.prof) {
+    std::vector<long long> hp(10 * nwarps);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(hp.data(), a.prof, sizeof(long long) * hp.size(), cudaMemcpyDeviceToHost);
+    cudaFree(a.prof);
+    const char* names[10] = {"A", "bar1", "B", "bar2", "C", "D1", "bar3", "D2+", "E", "-"};
+    for (int role = 0; role < team; ++role) {
+      double tot[10] = {0};
+      long long cnt = 0;
+      for (long long wv = role; wv < nwarps; wv += team, ++cnt)
+        for (int i = 0; i < 10; ++i) tot[i] += (double)hp[wv * 10 + i];
+      std::fprintf(stderr, "[bmc prof] team=%d ipc=%d warp-role %d cycles/iter:", team, ipc, role);
+      for (int i = 0; i < 9; ++i) std::fprintf(stderr, " %s=%.0f", names[i], tot[i] / cnt / (pr->iters + 1));
+      std::fprintf(stderr, "\n");
+    }
+  }
   return BMC_OK;
 }
 

@@ -76,6 +76,23 @@ __device__ __forceinline__ void team_sync(int team, int T) {
 
 constexpr int U_DOUBLES = 56;  // u_x[22], u_y[22], u_psi[11] (+pad)
 
+// Development aid (make PROFILE=1): per-warp cycle counts of each phase.
+#ifdef BMC_PROFILE
+struct PhaseClock {
+  long long acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = 0;
+};
+#define BMC_TICK(pc, i)                  \
+  do {                                   \
+    const long long t1_ = clock64();     \
+    (pc).acc[i] += t1_ - (pc).t0;        \
+    (pc).t0 = t1_;                       \
+  } while (0)
+#else
+struct PhaseClock {};
+#define BMC_TICK(pc, i) ((void)0)
+#endif
+
 // obstacles are padded to a multiple of JB with far-away, zero-radius dummies
 __host__ __device__ inline int pad_obstacles(int n) { return (n + JB - 1) / JB * JB; }
 
@@ -379,7 +396,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // keeps the 44 contraction accumulators out of the obstacle loop's registers.
 template <int M>
 __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, const float (&r)[M], WarpSmem* ws,
-                                              int lane, int w, int T, int team) {
+                                              int lane, int w, int T, int team, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
@@ -498,7 +515,9 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   }
   // The contraction is split by channel (T = 1: the warp does both in turn;
   // T >= 2: warps 0 and 1 own x and y), 22 fp64 accumulators per lane.
+  BMC_TICK(pc, 5);
   team_sync(team, T);   // D2 reads every warp's U
+  BMC_TICK(pc, 6);
   const double* __restrict__ Pt64 = pa.Pt64;
   // channel owners (T = 1: the warp owns both; T >= 2: warps 0 and 1) contract
   // their channel over every round
@@ -672,6 +691,10 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
     // (G15); every phase has a single call site so each is inlined once.
     // Team protocol per iteration: A (channel owners) | B (all, own rounds) |
     // C (all, redundant) + D1 (all, own rounds) | D2 + E (channel owners).
+    PhaseClock pc;
+#ifdef BMC_PROFILE
+    pc.t0 = clock64();
+#endif
 #pragma unroll 1
     for (int it = -1; it < K; ++it) {
 #pragma unroll
@@ -699,10 +722,14 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
         else if (k < NV2) ws->cf[2 * ch + 1][k - NV] = (float)xi[c];
         if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
+      BMC_TICK(pc, 0);
       team_sync(team, T);
+      BMC_TICK(pc, 1);
       // ---- B: heading target --------------------------------------------------
       phase_theta(Pt, Pt64, ws, lane, q, w, T);
+      BMC_TICK(pc, 2);
       team_sync(team, T);
+      BMC_TICK(pc, 3);
       // ---- C: xi2 step + lambda_psi (Eq. 19, 23b), every warp, same order ------
       double pth = 0.0;
       if (k < NV)
@@ -733,10 +760,12 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
         }
       }
       __syncwarp();
+      BMC_TICK(pc, 4);
       // ---- D: projections (own rounds) + contraction (owned channels) ---------
       const bool want_res = trace ? (it >= 0) : (it == K - 1);
-      phase_project<M>(want_res, pa, r, ws, lane, w, T, team);
+      phase_project<M>(want_res, pa, r, ws, lane, w, T, team, pc);
       __syncwarp();
+      BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
         r1sq = 0.f;
         rpsq = 0.f;
@@ -754,7 +783,12 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
         }
         if (trace && w == 0 && lane == 0 && active) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
       }
+      BMC_TICK(pc, 8);
     }
+#ifdef BMC_PROFILE
+    if (lane == 0 && a.prof)
+      for (int i = 0; i < 10; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * 10 + i] = pc.acc[i];
+#endif
     // ---- outputs ----------------------------------------------------------------
     if (active) {
       float* co = a.coeffs + l * 5 * NV;
