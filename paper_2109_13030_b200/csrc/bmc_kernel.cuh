@@ -358,8 +358,8 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
   const int nr = (q + 31) >> 5;
-#pragma unroll 1
-  for (int uu = 0; uu < QP / 32; ++uu) {
+#pragma unroll 2
+  for (int uu = 0; uu < QP / 32; ++uu) {   // two rounds in flight: independent atan2 chains
     const int u = (T - 1 - w) + uu * T;      // this warp's rounds (the leader gets the last, lightest)
     if (u >= nr) break;
     const int t = 32 * u + lane;
@@ -706,15 +706,14 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
           if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * ws->h[ch][k];
           __syncwarp();
           if (k < NV2) {
-            double a0 = ub[ch * NV2 + k], a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            // 8 independent fp64 chains (depth <= 6): the step is latency-bound
+            double acc[8] = {ub[ch * NV2 + k], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int j = 0; j < NV2; j += 2) {
-              a0 = fma(sf[BlobLayout::Mt + j * NV2 + k], ws->xi1[ch][j], a0);
-              a1 = fma(sf[BlobLayout::Mt + (j + 1) * NV2 + k], ws->xi1[ch][j + 1], a1);
-              b0 = fma(sf[BlobLayout::K11t + j * NV2 + k], ws->rhs[ch][j], b0);
-              b1 = fma(sf[BlobLayout::K11t + (j + 1) * NV2 + k], ws->rhs[ch][j + 1], b1);
+            for (int j = 0; j < NV2; ++j) {
+              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + k], ws->xi1[ch][j], acc[j & 3]);
+              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + k], ws->rhs[ch][j], acc[4 + (j & 3)]);
             }
-            xi[c] = (a0 + a1) + (b0 + b1);
+            xi[c] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
           }
           __syncwarp();
         }
@@ -738,25 +737,19 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
         if (k < NV) ws->rhspw[w][k] = lamp + rho_psi * pth;
         __syncwarp();
         if (k < NV) {
-          double s0 = ub[2 * NV2 + k], s1 = 0.0;
+          double s4[4] = {ub[2 * NV2 + k], 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < NV; j += 2) {
-            s0 = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhspw[w][j], s0);
-            if (j + 1 < NV) s1 = fma(sf[BlobLayout::Kp11t + (j + 1) * NV + k], ws->rhspw[w][j + 1], s1);
-          }
-          xi2r = s0 + s1;
+          for (int j = 0; j < NV; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhspw[w][j], s4[j & 3]);
+          xi2r = (s4[0] + s4[1]) + (s4[2] + s4[3]);
           ws->xi2w[w][k] = xi2r;
           ws->cf4[w][k] = (float)xi2r;
         }
         __syncwarp();
         if (k < NV) {
-          double g0 = 0.0, g1 = 0.0;
+          double g4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < NV; j += 2) {
-            g0 = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2w[w][j], g0);
-            if (j + 1 < NV) g1 = fma(sf[BlobLayout::Gppt + (j + 1) * NV + k], ws->xi2w[w][j + 1], g1);
-          }
-          lamp -= (g0 + g1) - rho_psi * pth;
+          for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2w[w][j], g4[j & 3]);
+          lamp -= ((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth;
         }
       }
       __syncwarp();
