@@ -19,7 +19,7 @@
 
 namespace bmc {
 cudaError_t launch_am(const KernelArgs& a, int wpc, cudaStream_t s);
-size_t kernel_smem_bytes(int QP, int n, int wpc);
+size_t kernel_smem_bytes(int QP, int n, int ipc, int team);
 }  // namespace bmc
 
 using namespace bmc;
@@ -239,15 +239,16 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->p.device);
   const int rounds = (c->q + 31) / 32;
-  int ipc = (int)std::min<int64_t>(16, (pr->B + dev_sms - 1) / dev_sms);
-  int team = std::max(1, std::min(rounds, 16 / std::max(1, ipc)));
+  int wmax = 16;   // resident warps per SM at the kernel's register budget
+  if (const char* s = std::getenv("BMC_WMAX")) wmax = std::max(1, std::min(32, std::atoi(s)));
+  int ipc = (int)std::min<int64_t>(wmax, (pr->B + dev_sms - 1) / dev_sms);
+  int team = std::max(1, std::min(rounds, wmax / std::max(1, ipc)));
   if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
   if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
   if (team < 1 || team > 4) team = 1;
-  if (team == 3) team = (ipc * 4 <= 16) ? 4 : 2;   // the D2 channel split needs T in {1, 2, 4}
-  if (ipc < 1 || ipc * team > 16) ipc = std::max(1, 16 / team);
-  while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024) --ipc;
-  if (kernel_smem_bytes(c->QP, pr->n_obs, ipc) > 227 * 1024)
+  if (ipc < 1 || ipc * team > 32) ipc = std::max(1, wmax / team);
+  while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024) --ipc;
+  if (kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024)
     return fail(BMC_EINVAL, "n_obs * q too large for shared memory");
   const int wpc = ipc;   // launch_am takes instances per CTA
   KernelArgs a;
@@ -306,24 +307,24 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   // development aid: BMC_PROF=1 with a PROFILE=1 build prints per-phase cycles
   const bool prof = std::getenv("BMC_PROF") != nullptr;
   const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
-  if (prof && cudaMalloc(&a.prof, sizeof(long long) * 10 * nwarps) == cudaSuccess)
-    cudaMemsetAsync(a.prof, 0, sizeof(long long) * 10 * nwarps, s);
+  if (prof && cudaMalloc(&a.prof, sizeof(long long) * 12 * nwarps) == cudaSuccess)
+    cudaMemsetAsync(a.prof, 0, sizeof(long long) * 12 * nwarps, s);
   cudaError_t e = launch_am(a, wpc, s);
   c->last_launches = 1;
   if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");
   if (prof && a.prof) {
-    std::vector<long long> hp(10 * nwarps);
+    std::vector<long long> hp(12 * nwarps);
     cudaStreamSynchronize(s);
     cudaMemcpy(hp.data(), a.prof, sizeof(long long) * hp.size(), cudaMemcpyDeviceToHost);
     cudaFree(a.prof);
-    const char* names[10] = {"A", "bar1", "B", "bar2", "C", "D1", "bar3", "D2+", "E", "-"};
+    const char* names[12] = {"A", "bar1", "B", "bar2", "C", "D2mma", "bar3", "D2+", "E", "tested", "D1", "needed"};
     for (int role = 0; role < team; ++role) {
-      double tot[10] = {0};
+      double tot[12] = {0};
       long long cnt = 0;
       for (long long wv = role; wv < nwarps; wv += team, ++cnt)
-        for (int i = 0; i < 10; ++i) tot[i] += (double)hp[wv * 10 + i];
+        for (int i = 0; i < 12; ++i) tot[i] += (double)hp[wv * 12 + i];
       std::fprintf(stderr, "[bmc prof] team=%d ipc=%d warp-role %d cycles/iter:", team, ipc, role);
-      for (int i = 0; i < 9; ++i) std::fprintf(stderr, " %s=%.0f", names[i], tot[i] / cnt / (pr->iters + 1));
+      for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.1f", names[i], tot[i] / cnt / (pr->iters + 1));
       std::fprintf(stderr, "\n");
     }
   }

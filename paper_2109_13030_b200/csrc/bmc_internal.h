@@ -37,10 +37,14 @@ struct BlobLayout {
   static constexpr int n_doubles_raw = Gdd + NV * NV;
   static constexpr int n_doubles = (n_doubles_raw + 1) & ~1;   // 16-byte multiple
   static constexpr size_t bytes_f64 = sizeof(double) * n_doubles;
-  // fp32 section: Pt[3][11][QP] = P, Pdot, Pddot transposed, zero for t >= q
-  BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * 3 * NV * (size_t)QP; }
-  // fp64 copy of the same basis for the F^T (F xi - g) and P^T theta contractions
-  BMC_HD static size_t bytes_p64(int QP) { return sizeof(double) * 3 * NV * (size_t)QP; }
+  // fp32 section: Pt[11][QP] = P transposed, zero for t >= q (Pdot = P Dm and
+  // Pddot = P Dm^2 are applied on the coefficient side, bmc_kernel.cuh dm_apply)
+  BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * NV * (size_t)QP; }
+  // fp64 copy of the same basis for the F^T (F xi - g) and P^T theta contractions,
+  // row stride QP + 4 doubles: the 8 rows of an FP64 MMA A-fragment then fall
+  // on distinct shared-memory banks
+  BMC_HD static int p64_stride(int QP) { return QP + 4; }
+  BMC_HD static size_t bytes_p64(int QP) { return sizeof(double) * NV * (size_t)p64_stride(QP); }
   BMC_HD static size_t bytes(int QP) { return bytes_f64 + bytes_f32(QP) + bytes_p64(QP); }
 };
 
@@ -86,8 +90,8 @@ struct SetupParams {
 struct HostConsts {
   int q, QP, nb, n, m;
   double blob_f64[BlobLayout::n_doubles];
-  float* pt = nullptr;     // [3][11][QP]
-  double* pt64 = nullptr;  // [3][11][QP]
+  float* pt = nullptr;     // [11][QP]
+  double* pt64 = nullptr;  // [11][p64_stride(QP)]
   ~HostConsts() { delete[] pt; delete[] pt64; }
 };
 

@@ -45,6 +45,9 @@ constexpr int QP = Q_MAX;   // sample stride of every per-sample smem array
 constexpr int JB = 8;       // obstacles per inside-test block
 
 constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per round
+constexpr int QP64 = QP + 4;     // row stride of the fp64 basis (BlobLayout::p64_stride)
+constexpr int QPU = QP + 4;      // row stride of WarpSmem::U
+constexpr int HP_SLOTS = 8 * 12; // per-warp partial contractions (D2), doubles
 
 // Per-instance state shared by the T warps of its team.  The x and y channels
 // of xi1 are decoupled in the xi1 step and the lambda step (Eq. 10: F and the
@@ -56,12 +59,19 @@ struct WarpSmem {
   double h[2][24];        // [ch][k] F^T (F xi1 - g) (fp64: it cancels), owner-written
   double xi2w[T_MAX][12]; // per-warp copies of xi2 (the heading step is redundant)
   double rhspw[T_MAX][12];
-  float cf[4][12];        // fp32: c_x - c_ref_x, c_c, c_y - c_ref_y, c_s (padded)
+  // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
+  // c_y - c_ref_y, Dm c_x, Dm c_y, Dm^2 c_x, Dm^2 c_y, c_c, c_s (Dm: the
+  // derivative operator on coefficients, Pdot = P Dm)
+  float cfi[NV + 1][8];
   float cf4[T_MAX][12];   // per-warp fp32 c_psi
   float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
   double part_th[T_MAX][16];    // per-warp P^T theta partials, summed in warp order
   float part_res[T_MAX][4];
-  float U[8][QP];               // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2)
+  float U[8][QP + 4];           // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2);
+                                // stride QP + 4: MMA B-fragment columns on distinct banks
+  float prv[3][QP];             // x, y, psi at the previous evaluation (culling clock)
+  float clk[T_MAX];             // per-round movement clocks (culling)
+  float pad_[T_MAX];
 };
 static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
 
@@ -74,12 +84,15 @@ __device__ __forceinline__ void team_sync(int team, int T) {
   }
 }
 
-constexpr int U_DOUBLES = 56;  // u_x[22], u_y[22], u_psi[11] (+pad)
+// u_x[22], u_y[22], u_psi[11] (+pad), then the per-lane weights of Dm and
+// Dm^T (DM_LO, DM_DI, DM_HI, DMT_LO, DMT_HI; [5][32], see dm_apply)
+constexpr int U_DOUBLES = 56 + 5 * 32;
+constexpr int DM_TAB = 56;
 
 // Development aid (make PROFILE=1): per-warp cycle counts of each phase.
 #ifdef BMC_PROFILE
 struct PhaseClock {
-  long long acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = 0;
 };
 #define BMC_TICK(pc, i)                  \
@@ -96,10 +109,19 @@ struct PhaseClock {};
 // obstacles are padded to a multiple of JB with far-away, zero-radius dummies
 __host__ __device__ inline int pad_obstacles(int n) { return (n + JB - 1) / JB * JB; }
 
-__host__ __device__ inline size_t smem_bytes(int n, int wpc) {
-  const int np = pad_obstacles(n);
+// clearance / active-list stride: padded obstacles + the far dummy, JB-aligned
+__host__ __device__ inline int clr_stride(int n) { return pad_obstacles(n) + JB; }
+
+// Layout after the constant blob: obstacles [npad + 1][QP] (row npad: the far
+// dummy), abi [npad + 1], u = K12 b, WarpSmem[ipc], clearance stamps
+// [ipc][4][nclr], active lists [ipc * T][nclr], D2 partials [ipc * T][HP_SLOTS],
+// mbarrier.
+__host__ __device__ inline size_t smem_bytes(int n, int ipc, int T) {
+  const int np = pad_obstacles(n) + 1;
   return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
-         U_DOUBLES * sizeof(double) + (size_t)wpc * sizeof(WarpSmem) + 16;
+         U_DOUBLES * sizeof(double) + (size_t)ipc * sizeof(WarpSmem) +
+         (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) + (size_t)ipc * T * HP_SLOTS * sizeof(double) +
+         16;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -137,6 +159,15 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// FP64 tensor-core MMA D = A B + D, m8n8k4 (A row-major 8x4, B col-major 4x8):
+// a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
+// d[i] = D[lane / 4][2 (lane % 4) + i].
+__device__ __forceinline__ void mma_f64_884(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
 // ------------------------------------------------------------ warp reductions
@@ -200,6 +231,31 @@ __device__ __forceinline__ V tr_reduce(V* v, int lane) {
   return v[0];
 }
 
+// Bernstein derivative on coefficients (degree n = 10, t in [0, T]):
+// Pdot = P Dm exactly, Dm tridiagonal with Dm[k][k-1] = -k / T,
+// Dm[k][k] = (2k - n) / T, Dm[k][k+1] = (n - k) / T (derivative of B_{k,n}
+// written in the degree-n basis by degree elevation).  Lane k < 11 holds
+// entry k; the per-lane weights (zero outside the band and for k >= 11) come
+// from the table staged in shared memory.
+__device__ __forceinline__ double band_apply(double c, const double* tab, int lo_row, int hi_row, int k) {
+  const double lo = __shfl_up_sync(FULL, c, 1), hi = __shfl_down_sync(FULL, c, 1);
+  return fma(tab[lo_row * 32 + k], lo, fma(tab[hi_row * 32 + k], hi, tab[1 * 32 + k] * c));
+}
+// (Dm c)_k = (-k c_{k-1} + (2k - n) c_k + (n - k) c_{k+1}) / T
+__device__ __forceinline__ double dm_apply(double c, const double* tab, int k) { return band_apply(c, tab, 0, 2, k); }
+// (Dm^T g)_k = ((n - k + 1) g_{k-1} + (2k - n) g_k - (k + 1) g_{k+1}) / T
+__device__ __forceinline__ double dmT_apply(double g, const double* tab, int k) { return band_apply(g, tab, 3, 4, k); }
+// the table: rows DM_LO, DM_DI, DM_HI, DMT_LO, DMT_HI over lanes 0..31
+__device__ __forceinline__ void dm_table(double* tab, int k, double T) {
+  const int n = NV - 1;
+  const bool in = k < NV;
+  tab[0 * 32 + k] = (in && k >= 1) ? -k / T : 0.0;
+  tab[1 * 32 + k] = in ? (2.0 * k - n) / T : 0.0;
+  tab[2 * 32 + k] = (in && k < n) ? (n - k) / T : 0.0;
+  tab[3 * 32 + k] = (in && k >= 1) ? (n - k + 1) / T : 0.0;
+  tab[4 * 32 + k] = (in && k < n) ? -(k + 1) / T : 0.0;
+}
+
 __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
   const float4 a = reinterpret_cast<const float4*>(src)[0];
   const float4 b = reinterpret_cast<const float4*>(src)[1];
@@ -217,8 +273,14 @@ struct Proj {
   const float4* abi;     // smem (a, b, a^2 or ab, kind) per obstacle
   int q, n, ntf, rtail, rounds;
   bool all_circ;
-  float nR1, nR2p1, v_max, a_max, vref_x, vref_y;
+  float nR1, nR2p1, v_max, a_max;
   float rlo, rhi;        // extent of the circle offsets along the heading
+  float rabs;            // max(|rlo|, |rhi|)
+  float* clr;            // smem clearance stamps of the instance, [4 rounds][nclr]
+  int* list;             // smem active list of the warp, [nclr]
+  int npad, nclr;        // padded obstacle count (index npad = far dummy), stride
+  double* hp;            // smem D2 partials of the team's warps, [T][HP_SLOTS]
+  const double* dmtab;   // smem weights of Dm, Dm^T (dm_table)
 };
 
 // --------------------------------------------------- collision projections
@@ -246,51 +308,50 @@ struct Proj {
 // r* = clamp(-B, rlo, rhi) -- a lower bound of every centre's distance, so the
 // test is conservative (exact cases only ever go to the second pass) and
 // costs the same for any number of circles.
-template <int M, bool SPLIT>
+//
+// Only the obstacles of the round's active list are visited (see
+// `build_active`); the pass records, per visited obstacle, the round's
+// clearance min_t |segment - o_j| - a_j stamped with the movement clock A.
+template <int M>
 __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
-                                          int n, int g, int S, const float (&X)[M], const float (&Y)[M],
+                                          const int* __restrict__ list, int na, float* __restrict__ clr, float A,
+                                          int lane, const float (&X)[M], const float (&Y)[M],
                                           float xc, float yc, float cu, float su, float rlo, float rhi,
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
-                                          float (&Dy)[M], float& rc) {
-  const int trips = SPLIT ? (n + S - 1) / S : pad_obstacles(n);
-  constexpr int NBK = 1;   // blocks per chunk (kept at 1: the hot loop must stay in the I-cache)
+                                          float (&Dy)[M], float& rc, long long* prof_need = nullptr) {
 #pragma unroll 1
-  for (int jc0 = 0; jc0 < trips; jc0 += NBK * JB) {
-    unsigned mask[NBK];
+  for (int jb = 0; jb < na; jb += JB) {
+    unsigned mask = 0u, qm = 0u;
 #pragma unroll
-    for (int bk = 0; bk < NBK; ++bk) {
-      mask[bk] = 0u;
-      const int jb = jc0 + bk * JB;
-      if (jb < trips) {
-#pragma unroll
-        for (int jj = 0; jj < JB; ++jj) {
-          const int it = jb + jj;
-          const int j = SPLIT ? g + it * S : it;   // unsplit: the padding makes every slot valid
-          const bool have = !SPLIT || ((it < trips) && (j < n));
-          const int jcl = have ? j : 0;
-          const float2 o = ob[jcl * QP];
-          const float a2 = abi[jcl].z;
-          const float dx = xc - o.x, dy = yc - o.y;
-          const float d0 = fmaf(dy, dy, dx * dx), bd = fmaf(dy, su, dx * cu);
-          const float rs = fmaxf(rlo, fminf(rhi, -bd));
-          const float qmin = fmaf(rs, fmaf(2.f, bd, rs), d0);
-          // margin: absolute rounding of qmin is < 1e-6 m^2 for any obstacle within reach
-          mask[bk] |= (have && qmin < fmaf(a2, 1.00001f, 1e-5f)) ? (1u << jj) : 0u;
-        }
-      }
+    for (int jj = 0; jj < JB; ++jj) {
+      const int j = list[jb + jj];   // the list is padded to a multiple of JB with a far dummy
+      const float2 o = ob[j * QP];
+      const float a2 = abi[j].z;
+      const float dx = xc - o.x, dy = yc - o.y;
+      const float d0 = fmaf(dy, dy, dx * dx), bd = fmaf(dy, su, dx * cu);
+      const float rs = fmaxf(rlo, fminf(rhi, -bd));
+      const float qmin = fmaf(rs, fmaf(2.f, bd, rs), d0);
+      // margin: absolute rounding of qmin is < 1e-6 m^2 for any obstacle within reach
+      mask |= (qmin < fmaf(a2, 1.00001f, 1e-5f)) ? (1u << jj) : 0u;
+      // round minimum of qmin (non-negative floats order as their bit patterns)
+      const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(fmaxf(qmin, 0.f)));
+      qm = (lane == jj) ? mn : qm;
     }
-    unsigned need[NBK];
-#pragma unroll
-    for (int bk = 0; bk < NBK; ++bk) need[bk] = __reduce_or_sync(FULL, mask[bk]);
-#pragma unroll
-    for (int bk = 0; bk < NBK; ++bk) {
-      unsigned nd = need[bk];
+    if (lane < JB) {
+      const int j = list[jb + lane];
+      clr[j] = sqrtf(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
+    }
+    const unsigned need = __reduce_or_sync(FULL, mask);
+#ifdef BMC_PROFILE
+    if (prof_need) *prof_need += __popc(need);
+#endif
+    {
+      unsigned nd = need;
       while (nd) {
         const int jj = __ffs(nd) - 1;
         nd &= nd - 1;
-        const int it = jc0 + bk * JB + jj;
-        const int j = SPLIT ? g + it * S : it;
-        if ((mask[bk] >> jj) & 1u) {
+        const int j = list[jb + jj];
+        if ((mask >> jj) & 1u) {
           const float2 o = ob[j * QP];
           const float a = abi[j].x;
 #pragma unroll
@@ -346,14 +407,68 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
   }
 }
 
+// ------------------------------------------------------ temporal culling
+// Every iteration moves the circle centres of sample t by at most
+//   |(dx, dy)| + max(|rlo|, |rhi|) |dpsi|        (|d cos psi| <= |d psi|)
+// where (dx, dy, dpsi) is the change of the evaluated x, y, psi since the
+// previous evaluation.  A per-(instance, round) clock A sums the warp maximum of
+// this bound over the iterations.  An obstacle whose stamped clearance
+// (coll_circ) still exceeds the movement since its stamp plus CULL_MARGIN
+// cannot have any circle inside it in this round, so its contribution is
+// exactly zero and it is skipped: the result is bitwise that of testing it.
+// The margin covers the fp32 rounding of the evaluated samples (< 1e-4 m for
+// deviations up to 1 km).
+constexpr float CULL_MARGIN = 2e-3f;
+
+// advance the round's clock by this evaluation's movement; returns the clock
+__device__ __forceinline__ float cull_tick(WarpSmem* ws, int u, int t, float x, float y, float psi, float rabs,
+                                           int lane) {
+  const float dx = x - ws->prv[0][t], dy = y - ws->prv[1][t], dp = psi - ws->prv[2][t];
+  ws->prv[0][t] = x;
+  ws->prv[1][t] = y;
+  ws->prv[2][t] = psi;
+  // |.| of a NaN keeps a NaN bit pattern, which is above +inf: the clock becomes NaN
+  const float mv = fmaf(rabs, fabsf(dp), sqrtf(fmaf(dx, dx, dy * dy)));
+  const float mx = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(fabsf(mv))));
+  const float A = ws->clk[u] + mx;
+  __syncwarp();
+  if (lane == 0) ws->clk[u] = A;
+  return A;
+}
+
+// Active list of one round: obstacles whose clearance no longer covers the
+// movement since it was stamped, padded to a multiple of JB with the far dummy
+// `npad`.  Returns the padded length.
+__device__ __forceinline__ int build_active(const float* __restrict__ clr, int* __restrict__ list, int npad,
+                                            float A, int lane) {
+  int na = 0;
+  const float lim = A + CULL_MARGIN;
+#pragma unroll 1
+  for (int j0 = 0; j0 < npad; j0 += 32) {
+    const int j = j0 + lane;
+    const bool act = (j < npad) && !(clr[j] > lim);   // NaN clock or stamp: active
+    const unsigned bal = __ballot_sync(FULL, act);
+    if (act) list[na + __popc(bal & ((1u << lane) - 1u))] = j;
+    na += __popc(bal);
+  }
+  const int nap = (na + JB - 1) & ~(JB - 1);
+  if (lane < nap - na) list[na + lane] = npad;
+  __syncwarp();
+  return nap;
+}
+
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
 __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
                                             WarpSmem* ws, int lane, int q, int w, int T) {
   float cc[NV], cs[NV];
-  load12(ws->cf[1], cc);
-  load12(ws->cf[3], cs);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const float2 v = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
+    cc[k] = v.x;
+    cs[k] = v.y;
+  }
   double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
@@ -378,7 +493,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     ws->th[t] = tht;
     const double thd = (double)tht;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP + t], thd, acc[k]);
+    for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
   }
   // 11 entries as 8 + 4 transpose-reduce slots
   const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
@@ -392,8 +507,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // collision projections, and the per-sample vectors of h = F^T (F xi1 - g)
 //   U0 = n R1 e_c - D_x, U1 = (n R2 + 1) e_c - E_x, U2, U3 likewise for y,
 //   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
-// written to shared memory; D2: contraction with P, Pdot, Pddot.  Splitting
-// keeps the 44 contraction accumulators out of the obstacle loop's registers.
+// written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
 template <int M>
 __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, const float (&r)[M], WarpSmem* ws,
                                               int lane, int w, int T, int team, PhaseClock& pc) {
@@ -411,22 +525,23 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     }
     const bool own = (g == 0);               // group 0 owns the sample's contributions
     const bool valid = own && (t < q);
-    float x = 0.f, y = 0.f, xd = pa.vref_x, yd = pa.vref_y, xdd = 0.f, ydd = 0.f, psi = 0.f;
+    // x = P c, xdot = Pdot c = P (Dm c), xddot = P (Dm^2 c): one basis row per k
+    float x = 0.f, y = 0.f, xd = 0.f, yd = 0.f, xdd = 0.f, ydd = 0.f, psi = 0.f;
     {
-      float cx[NV], cy[NV], cp[NV];
-      load12(ws->cf[0], cx);
-      load12(ws->cf[2], cy);
+      float cp[NV];
       load12(ws->cf4[w], cp);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        const float p = Pt[k * QP + t], pd = Pt[(NV + k) * QP + t], pdd = Pt[(2 * NV + k) * QP + t];
-        x = fmaf(p, cx[k], x);
-        y = fmaf(p, cy[k], y);
+        const float p = Pt[k * QP + t];
+        const float4 c0 = *reinterpret_cast<const float4*>(&ws->cfi[k][0]);
+        const float2 c1 = *reinterpret_cast<const float2*>(&ws->cfi[k][4]);
+        x = fmaf(p, c0.x, x);
+        y = fmaf(p, c0.y, y);
+        xd = fmaf(p, c0.z, xd);
+        yd = fmaf(p, c0.w, yd);
+        xdd = fmaf(p, c1.x, xdd);
+        ydd = fmaf(p, c1.y, ydd);
         psi = fmaf(p, cp[k], psi);
-        xd = fmaf(pd, cx[k], xd);
-        yd = fmaf(pd, cy[k], yd);
-        xdd = fmaf(pdd, cx[k], xdd);
-        ydd = fmaf(pdd, cy[k], ydd);
       }
     }
     // velocity / acceleration: g = projection onto the bound disk (G6, G7)
@@ -451,22 +566,39 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     }
     float rc = 0.f;
     const float2* ob = pa.obs + t;
-    if (pa.all_circ) {
-      if (S == 1)
-        coll_circ<M, false>(RES, ob, pa.abi, n, 0, 1, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s, Dx, Dy, rc);
-      else   // split tail round: few obstacles per lane, the plain loop is smaller code
-        coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
-    } else {
-      coll_general<M>(RES, false, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+    // circular obstacles in a full round: culled, blocked inside test
+    // (coll_circ); otherwise (ellipses, split tail round: few obstacles per
+    // lane) the plain loop.  A non-finite result (x~ = y~ = 0 exactly, G18,
+    // rare) reruns the plain loop with the guard; one call site keeps the
+    // hot loop small in the instruction cache.
+    bool general = !(pa.all_circ && S == 1);
+    if (!general) {
+      float* clr = pa.clr + u * pa.nclr;
+      const float A = cull_tick(ws, u, t, x, y, psi, pa.rabs, lane);
+      const int na = build_active(clr, pa.list, pa.npad, A, lane);
+#ifdef BMC_PROFILE
+      pc.acc[9] += na;
+#endif
+      long long* pneed = nullptr;
+#ifdef BMC_PROFILE
+      pneed = &pc.acc[11];
+#endif
+      coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s,
+                   Dx, Dy, rc, pneed);
     }
-    float chk = rc;
+    bool guard = false;
+#pragma unroll 1
+    for (;;) {
+      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      float chk = rc;
 #pragma unroll
-    for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
-    if (__any_sync(FULL, !isfinite(chk))) {   // rare: x~ = y~ = 0 exactly (G18)
+      for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
+      if (guard || !__any_sync(FULL, !isfinite(chk))) break;
 #pragma unroll
       for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
       rc = 0.f;
-      coll_general<M>(RES, true, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      guard = true;
+      general = true;
     }
     for (int off = R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
 #pragma unroll
@@ -501,10 +633,43 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     }
   }
   __syncwarp();
-  // D2: h partial over this warp's samples (the basis is zero for t >= q).
-  // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so the
-  // sum over samples cancels and fp32 accumulation would dominate the error
-  // (DESIGN.md "Numerics").
+  BMC_TICK(pc, 10);
+  // D2: partial G = P^T U over this warp's own samples on the FP64 tensor
+  // cores (q x 11 basis, U = [U0 .. U7]: 11 x 8 outputs, all of them used):
+  // two m8n8k4 row tiles (basis rows 0..15, rows >= 11 clamped and
+  // discarded), k = 4 samples per step.  The Pdot / Pddot terms follow from
+  // G through Pdot^T u = Dm^T (P^T u) (see dm_apply), after the team sum.
+  // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so
+  // the sum over samples cancels and fp32 accumulation would dominate the
+  // error.  Each warp contracts the samples it
+  // projected itself, so no team barrier separates D1 from D2.
+  {
+    const double* __restrict__ P64 = pa.Pt64;
+    const int g8 = lane >> 2, c4 = lane & 3;   // fragment row / column group
+    const int aoff0 = g8 * QP64 + c4, aoff1 = min(8 + g8, NV - 1) * QP64 + c4;
+    const float* __restrict__ ucol = &ws->U[g8][c4];   // B fragment: U[k = c4][n = g8]
+    double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+#pragma unroll 1
+    for (int u = T - 1 - w; u < pa.rounds; u += T) {
+      const int t0 = 32 * u;
+      const int ns = (u < pa.ntf) ? 8 : ((q - t0 + 3) >> 2);
+#pragma unroll 4
+      for (int st = 0; st < ns; ++st) {
+        const int t = t0 + 4 * st;
+        const double b = (double)ucol[t];
+        mma_f64_884(g0, P64[aoff0 + t], b);
+        mma_f64_884(g1, P64[aoff1 + t], b);
+      }
+    }
+    // C fragment: G[row g8 (+ 8)][column 2 c4 + i] -> partial slots [column][row]
+    double* hp = pa.hp + w * HP_SLOTS;
+    hp[(2 * c4) * 12 + g8] = g0[0];
+    hp[(2 * c4 + 1) * 12 + g8] = g0[1];
+    if (8 + g8 < NV) {
+      hp[(2 * c4) * 12 + 8 + g8] = g1[0];
+      hp[(2 * c4 + 1) * 12 + 8 + g8] = g1[1];
+    }
+  }
   if (RES) {   // residual partials must be visible to the team before the barrier
     res = warp_sum(res);
     rps = warp_sum(rps);
@@ -513,45 +678,48 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       ws->part_res[w][1] = rps;
     }
   }
-  // The contraction is split by channel (T = 1: the warp does both in turn;
-  // T >= 2: warps 0 and 1 own x and y), 22 fp64 accumulators per lane.
   BMC_TICK(pc, 5);
-  team_sync(team, T);   // D2 reads every warp's U
+  team_sync(team, T);   // every warp's partials are in place
   BMC_TICK(pc, 6);
-  const double* __restrict__ Pt64 = pa.Pt64;
-  // channel owners (T = 1: the warp owns both; T >= 2: warps 0 and 1) contract
-  // their channel over every round
+  // channel owners (T = 1: the warp owns both; T >= 2: warps 0 and 1) sum the
+  // team's partials in warp order and assemble
+  //   h_pos  = P^T U0 + Dm^T (P^T U4) + Dm^T Dm^T (P^T U5)   (x; y: U2, U6, U7)
+  //   h_copy = P^T U1                                          (x; y: U3)
   const int nch = (T == 1) ? 2 : (w < 2 ? 1 : 0);
+  const int k = lane;
 #pragma unroll 1
   for (int ci = 0; ci < nch; ++ci) {
     const int ch = (T == 1) ? ci : w;
-    double acc[24];
+    // lanes k < 11: (P^T U)[k] of U0/U2 (gp), U4/U6 (gv), U5/U7 (ga);
+    // lanes 11..21: gp = (P^T U1/U3)[k - 11].  Branch-free: other lanes read
+    // clamped slots and meet zero weights in dmT_apply.
+    const int kk = (k < NV) ? k : min(k - NV, NV - 1);
+    const int colp = (k < NV) ? 2 * ch : 2 * ch + 1;
+    double gp = 0.0, gv = 0.0, ga = 0.0;
 #pragma unroll
-    for (int k = 0; k < 24; ++k) acc[k] = 0.0;
-#pragma unroll 1
-    for (int u = 0; u < pa.rounds; ++u) {
-      const int t = 32 * u + lane;
-      // channel x: U0 (P), U1 (copy, P), U4 (Pdot), U5 (Pddot); channel y: U2, U3, U6, U7
-      const double ua = ws->U[2 * ch][t], ub = ws->U[2 * ch + 1][t];
-      const double uv = ws->U[4 + 2 * ch][t], uac = ws->U[5 + 2 * ch][t];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const double p = Pt64[k * QP + t], pd = Pt64[(NV + k) * QP + t], pdd = Pt64[(2 * NV + k) * QP + t];
-        acc[k] = fma(p, ua, fma(pd, uv, fma(pdd, uac, acc[k])));
-        acc[NV + k] = fma(p, ub, acc[NV + k]);
+    for (int ww = 0; ww < T_MAX; ++ww) {
+      if (ww < T) {
+        const double* hp = pa.hp + ww * HP_SLOTS;
+        gp += hp[colp * 12 + kk];
+        gv += hp[(4 + 2 * ch) * 12 + kk];
+        ga += hp[(5 + 2 * ch) * 12 + kk];
       }
     }
-    // 22 entries as 16 + 8 transpose-reduce slots (22 + 3 butterflies, not 31)
-    const double v16 = tr_reduce<16>(acc, lane);       // entry lane >> 1
-    const double v8 = tr_reduce<8>(acc + 16, lane);    // entry 16 + (lane >> 2)
-    if (!(lane & 1)) ws->h[ch][lane >> 1] = v16;
-    if (!(lane & 3) && 16 + (lane >> 2) < NV2) ws->h[ch][16 + (lane >> 2)] = v8;
+    // Dm^T gv + Dm^T Dm^T ga = Dm^T (gv + Dm^T ga)
+    const double z = dmT_apply(ga, pa.dmtab, k) + gv;
+    const double d = dmT_apply(z, pa.dmtab, k);
+    if (k < NV2) ws->h[ch][k] = (k < NV) ? gp + d : gp;
   }
 }
 
 // ---------------------------------------------------------------- kernel
+#ifdef BMC_MAXNREG   // experiments: register cap below the 128 of 16 warps per SM
+#define BMC_KERNEL_BOUNDS __maxnreg__(BMC_MAXNREG)
+#else
+#define BMC_KERNEL_BOUNDS __launch_bounds__(512)
+#endif
 template <int M>
-__global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ KernelArgs a) {
+__global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
   const int n = a.n, q = a.q, K = a.iters;
@@ -559,13 +727,16 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   const float* Pt = reinterpret_cast<const float*>(smem + BlobLayout::bytes_f64);
   const double* Pt64 = reinterpret_cast<const double*>(smem + BlobLayout::bytes_f64 + BlobLayout::bytes_f32(QP));
   float2* obs = reinterpret_cast<float2*>(smem + BlobLayout::bytes(QP));
-  const int npad = pad_obstacles(n);
-  float4* abi = reinterpret_cast<float4*>(obs + (size_t)npad * QP);
-  double* ub = reinterpret_cast<double*>(abi + npad);
+  const int npad = pad_obstacles(n), nclr = clr_stride(n);
+  float4* abi = reinterpret_cast<float4*>(obs + (size_t)(npad + 1) * QP);
+  double* ub = reinterpret_cast<double*>(abi + npad + 1);
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
   const int T = a.team, ipc = wpc / T;               // warps per instance, instances per CTA
   const int team = warp / T, w = warp - team * T;    // instance slot in the CTA, rank in the team
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(wsbase + ipc);
+  float* clr_base = reinterpret_cast<float*>(wsbase + ipc);
+  int* list_base = reinterpret_cast<int*>(clr_base + (size_t)ipc * T_MAX * nclr);
+  double* hp_base = reinterpret_cast<double*>(list_base + (size_t)wpc * nclr);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (size_t)wpc * HP_SLOTS);
 
   // --- stage the batch-invariant data -------------------------------------
   if (tid == 0) mbar_init(mbar, 1);
@@ -582,7 +753,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   // obstacles relative to the boundary line (x_ref(t), y_ref(t)), computed in
   // fp64 and rounded once; padding samples far away
   const double inv_q1 = 1.0 / (double)(q - 1);
-  for (int idx = tid; idx < npad * QP; idx += blockDim.x) {
+  for (int idx = tid; idx < (npad + 1) * QP; idx += blockDim.x) {
     const int j = idx / QP, t = idx - j * QP;
     float2 v = make_float2(1.0e4f, 1.0e4f);
     if (t < q && j < n) {
@@ -593,20 +764,25 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
     obs[idx] = v;
   }
   int circ = 1;
-  for (int j = n + tid; j < npad; j += blockDim.x) abi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = n + tid; j <= npad; j += blockDim.x) abi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = tid; i < ipc * T_MAX * nclr; i += blockDim.x) clr_base[i] = -1.0e30f;   // never tested
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
     abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
     circ &= (aa == bb);
   }
-  for (int i = tid; i < ipc * 4 * 12; i += blockDim.x) (&wsbase[i / 48].cf[0][0])[i % 48] = 0.f;
+  for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
+    (&wsbase[i / ((NV + 1) * 8)].cfi[0][0])[i % ((NV + 1) * 8)] = 0.f;
   for (int i = tid; i < ipc * T_MAX * 12; i += blockDim.x)
     (&wsbase[i / (T_MAX * 12)].cf4[0][0])[i % (T_MAX * 12)] = 0.f;
-  for (int i = tid; i < ipc * 8 * QP; i += blockDim.x) (&wsbase[i / (8 * QP)].U[0][0])[i % (8 * QP)] = 0.f;
+  for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
+  for (int i = tid; i < ipc * (3 * QP + 2 * T_MAX); i += blockDim.x)
+    (&wsbase[i / (3 * QP + 2 * T_MAX)].prv[0][0])[i % (3 * QP + 2 * T_MAX)] = 0.f;
   const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
   __syncthreads();
+  if (tid < 32) dm_table(ub + DM_TAB, tid, a.T);
   if (tid < NV2) {   // u = K12 b per channel (boundary part of Eq. 4)
     double sx = 0.0, sy = 0.0;
     for (int rr = 0; rr < a.nb; ++rr) {
@@ -643,14 +819,19 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   pa.nR2p1 = a.nR2p1;
   pa.v_max = a.v_max;
   pa.a_max = a.a_max;
-  pa.vref_x = (float)(a.ref_dx / a.T);
-  pa.vref_y = (float)(a.ref_dy / a.T);
   pa.rlo = a.r[0];
   pa.rhi = a.r[0];
   for (int i = 1; i < M; ++i) {
     pa.rlo = fminf(pa.rlo, a.r[i]);
     pa.rhi = fmaxf(pa.rhi, a.r[i]);
   }
+  pa.rabs = fmaxf(fabsf(pa.rlo), fabsf(pa.rhi));
+  pa.npad = npad;
+  pa.nclr = nclr;
+  pa.clr = clr_base + (size_t)team * T_MAX * nclr;
+  pa.list = list_base + (size_t)warp * nclr;
+  pa.hp = hp_base + (size_t)team * T * HP_SLOTS;
+  pa.dmtab = ub + DM_TAB;
   float r[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
@@ -665,6 +846,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
   {
     const int k = lane;
     const double rho = a.rho, rho_psi = a.rho_psi;
+    const double* dmtab = ub + DM_TAB;
     // channels owned by this warp (phases A, D2, E): both for T = 1, channel w for w < 2
     const int nown = (T == 1) ? 2 : (w < 2 ? 1 : 0);
     const int chb = (T == 1) ? 0 : w;
@@ -703,22 +885,37 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
         const int ch = chb + c;
         if (it >= 0) {
           // ---- A: xi1 step, Eq. 13/17 via Eq. 4 (fp64) ---------------------
+          // every lane runs row min(k, 21) (no divergent branch); lanes >= 22 keep 0
+          const int kc = min(k, NV2 - 1);
           if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * ws->h[ch][k];
           __syncwarp();
-          if (k < NV2) {
+          {
             // 8 independent fp64 chains (depth <= 6): the step is latency-bound
-            double acc[8] = {ub[ch * NV2 + k], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int j = 0; j < NV2; ++j) {
-              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + k], ws->xi1[ch][j], acc[j & 3]);
-              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + k], ws->rhs[ch][j], acc[4 + (j & 3)]);
+              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
+              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
             }
-            xi[c] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+            xi[c] = (k < NV2) ? v : 0.0;
           }
           __syncwarp();
         }
-        if (k < NV) ws->cf[2 * ch][k] = (float)(xi[c] - cref[c]);
-        else if (k < NV2) ws->cf[2 * ch + 1][k - NV] = (float)xi[c];
+        {
+          // position (deviation from the boundary line), Dm c and Dm^2 c in fp64
+          // (Dm tridiagonal: (Dm c)_k = (-k c_{k-1} + (2k - n) c_k + (n - k) c_{k+1}) / T,
+          // n = 10; lanes >= 11 hold the copy block and meet zero weights)
+          const double d1 = dm_apply(xi[c], dmtab, k);
+          const double d2 = dm_apply(d1, dmtab, k);
+          if (k < NV) {
+            ws->cfi[k][ch] = (float)(xi[c] - cref[c]);
+            ws->cfi[k][2 + ch] = (float)d1;
+            ws->cfi[k][4 + ch] = (float)d2;
+          } else if (k < NV2) {
+            ws->cfi[k - NV][6 + ch] = (float)xi[c];
+          }
+        }
         if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
       BMC_TICK(pc, 0);
@@ -730,26 +927,33 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
       team_sync(team, T);
       BMC_TICK(pc, 3);
       // ---- C: xi2 step + lambda_psi (Eq. 19, 23b), every warp, same order ------
+      // lanes run row min(k, 10) without divergent branches; lanes >= 11 keep 0
+      const int k1 = min(k, NV - 1);
       double pth = 0.0;
-      if (k < NV)
-        for (int ww = 0; ww < T; ++ww) pth += ws->part_th[ww][k];
+#pragma unroll
+      for (int ww = 0; ww < T_MAX; ++ww)
+        if (ww < T) pth += ws->part_th[ww][k1];
       if (it >= 0) {
         if (k < NV) ws->rhspw[w][k] = lamp + rho_psi * pth;
         __syncwarp();
-        if (k < NV) {
-          double s4[4] = {ub[2 * NV2 + k], 0.0, 0.0, 0.0};
+        {
+          double s4[4] = {ub[2 * NV2 + k1], 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < NV; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k], ws->rhspw[w][j], s4[j & 3]);
-          xi2r = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-          ws->xi2w[w][k] = xi2r;
-          ws->cf4[w][k] = (float)xi2r;
+          for (int j = 0; j < NV; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k1], ws->rhspw[w][j], s4[j & 3]);
+          const double v = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          xi2r = (k < NV) ? v : 0.0;
+          if (k < NV) {
+            ws->xi2w[w][k] = xi2r;
+            ws->cf4[w][k] = (float)xi2r;
+          }
         }
         __syncwarp();
-        if (k < NV) {
+        {
           double g4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k], ws->xi2w[w][j], g4[j & 3]);
-          lamp -= ((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth;
+          for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
+          const double v = lamp - (((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth);
+          lamp = (k < NV) ? v : 0.0;
         }
       }
       __syncwarp();
@@ -780,7 +984,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
     }
 #ifdef BMC_PROFILE
     if (lane == 0 && a.prof)
-      for (int i = 0; i < 10; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * 10 + i] = pc.acc[i];
+      for (int i = 0; i < 12; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * 12 + i] = pc.acc[i];
 #endif
     // ---- outputs ----------------------------------------------------------------
     if (active) {
@@ -854,7 +1058,7 @@ __global__ void __launch_bounds__(512) bmc_am_kernel(const __grid_constant__ Ker
 
 }  // namespace
 
-size_t kernel_smem_bytes(int QPx, int n, int wpc);
+size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 
 // One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
 // this; bmc_launch.cu dispatches on m.
@@ -867,7 +1071,7 @@ cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const size_t smem = smem_bytes(a.n, ipc);
+  const size_t smem = smem_bytes(a.n, ipc, a.team);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
   bmc_am_kernel<M><<<grid, 32 * a.team * ipc, smem, s>>>(a);
   return cudaGetLastError();

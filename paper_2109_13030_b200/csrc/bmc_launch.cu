@@ -12,7 +12,7 @@ extern template cudaError_t launch_am_m<6>(const KernelArgs&, int, cudaStream_t)
 extern template cudaError_t launch_am_m<7>(const KernelArgs&, int, cudaStream_t);
 extern template cudaError_t launch_am_m<8>(const KernelArgs&, int, cudaStream_t);
 
-size_t kernel_smem_bytes(int /*QP: fixed Q_MAX*/, int n, int wpc) { return smem_bytes(n, wpc); }
+size_t kernel_smem_bytes(int /*QP: fixed Q_MAX*/, int n, int ipc, int team) { return smem_bytes(n, ipc, team); }
 
 cudaError_t launch_am(const KernelArgs& a, int wpc, cudaStream_t s) {
   switch (a.m) {

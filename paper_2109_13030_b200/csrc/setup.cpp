@@ -20,6 +20,7 @@
 //        xi1' = K11 (lambda + rho F^T g) + K12 b
 //             = M xi1 + K11 (lambda - rho h) + K12 b,   h = F^T (F xi1 - g)
 //    never forms F^T g from large absolute positions.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -190,18 +191,46 @@ int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err)
   }
   delete[] out->pt;
   delete[] out->pt64;
-  out->pt = new float[3 * NV * QP];
-  out->pt64 = new double[3 * NV * QP];
-  std::memset(out->pt, 0, sizeof(float) * 3 * NV * QP);
-  std::memset(out->pt64, 0, sizeof(double) * 3 * NV * QP);
+  const int S64 = BlobLayout::p64_stride(QP);
+  out->pt = new float[NV * QP];
+  out->pt64 = new double[NV * S64];
+  std::memset(out->pt, 0, sizeof(float) * NV * QP);
+  std::memset(out->pt64, 0, sizeof(double) * NV * S64);
   for (int k = 0; k < NV; ++k)
     for (int t = 0; t < q; ++t) {
-      const double v[3] = {P[t * NV + k], Pd[t * NV + k], Pdd[t * NV + k]};
-      for (int b = 0; b < 3; ++b) {
-        out->pt[(b * NV + k) * QP + t] = (float)v[b];
-        out->pt64[(b * NV + k) * QP + t] = v[b];
-      }
+      out->pt[k * QP + t] = (float)P[t * NV + k];
+      out->pt64[k * S64 + t] = P[t * NV + k];
     }
+  // The kernel evaluates Pdot c as P (Dm c) and Pdot^T u as Dm^T (P^T u) with the
+  // tridiagonal Dm of bmc_kernel.cuh (dm_apply); check the identity Pdot = P Dm,
+  // Pddot = P Dm^2 on this grid (it is exact up to rounding).
+  {
+    double dev = 0.0, scale = 0.0;
+    for (int t = 0; t < q; ++t)
+      for (int k = 0; k < NV; ++k) {
+        double d1 = 0.0, d2 = 0.0;
+        for (int j = std::max(0, k - 2); j <= std::min(deg, k + 2); ++j) {
+          // (Dm)[j][k] and (Dm^2)[j][k]
+          auto dm = [&](int r, int c) -> double {
+            if (c == r - 1) return -r / p.T;
+            if (c == r) return (2.0 * r - deg) / p.T;
+            if (c == r + 1) return (deg - r) / p.T;
+            return 0.0;
+          };
+          double dm2 = 0.0;
+          for (int i = std::max(0, j - 1); i <= std::min(deg, j + 1); ++i) dm2 += dm(j, i) * dm(i, k);
+          d1 += P[t * NV + j] * dm(j, k);
+          d2 += P[t * NV + j] * dm2;
+        }
+        dev = std::fmax(dev, std::fmax(std::fabs(d1 - Pd[t * NV + k]) * p.T,
+                                       std::fabs(d2 - Pdd[t * NV + k]) * p.T * p.T));
+        scale = std::fmax(scale, std::fmax(std::fabs(Pd[t * NV + k]) * p.T, std::fabs(Pdd[t * NV + k]) * p.T * p.T));
+      }
+    if (!(dev <= 1e-12 * scale)) {
+      if (err) *err = "internal: Bernstein derivative identity check failed";
+      return 2;
+    }
+  }
   return 0;
 }
 

@@ -3,7 +3,9 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from synth import CONFIGS, make_problem
-from paper_2109_13030_b200 import solver_for
+from paper_2109_13030_b200 import solver_for, bmc
+if os.environ.get("BMC_LIB"):   # experiments: a variant build (make TAG=...)
+    bmc.load_library(os.path.abspath(os.environ["BMC_LIB"]))
 torch.cuda.set_device(0)
 cfg = CONFIGS[sys.argv[1]]
 if len(sys.argv) > 2: cfg = cfg.with_(B=int(sys.argv[2]))
@@ -18,5 +20,5 @@ for _ in range(10):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); s.solve(*args, out=out); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print(f"{cfg.name} B={cfg.B} team={os.environ.get('BMC_TEAM','1')} ipc={os.environ.get('BMC_IPC','-')}: "
+print(f"{os.environ.get('BMC_LIB', '')} {cfg.name} B={cfg.B} wmax={os.environ.get('BMC_WMAX', '-')} team={os.environ.get('BMC_TEAM','1')} ipc={os.environ.get('BMC_IPC','-')}: "
       f"{min(ts):.3f} ms (med {np.median(ts):.3f})  best={int(out['best'][0])}  cost0={float(out['cost'][0]):.6f}")
