@@ -1,20 +1,18 @@
 // bmc_kernel.cuh -- fused batched AM iteration of arXiv 2109.13030 on sm_100a.
 //
-// One warp owns one batch instance l for all K iterations (instances are
-// independent, "each instance in the batch is independent"); a CTA of
-// WPC warps shares one shared-memory copy of the batch-invariant data: the
-// basis P, Pdot, Pddot and the KKT inverses (bulk-copied by TMA,
+// A team of T warps (1..4) owns one batch instance l for all K iterations
+// (instances are independent, "each instance in the batch is
+// independent"); a CTA of ipc teams shares one shared-memory copy of the
+// batch-invariant data: the basis P and the KKT inverses (bulk-copied by TMA,
 // cp.async.bulk + mbarrier) and the obstacle trajectories.
 //
-// Time samples are processed in rounds of 32 lanes (t = 32 u + lane).  The
-// last, partial round (q mod 32 samples) splits the obstacles over lane
-// groups instead of idling lanes: R = next_pow2(q mod 32) lanes per group,
-// S = 32 / R groups, group g takes obstacles j = g, g + S, ..., and the
-// per-sample sums are combined by xor-shuffles across groups.
+// Time samples are processed in rounds of 32 lanes (t = 32 u + lane); warp w
+// of a team takes rounds u = T-1-w, 2T-1-w, ...  Samples t >= q of the last
+// round have a zero basis row and far-away obstacle slots and drop out.
 //
 // Per iteration (paper step order):
 //   A  xi1 step (Eq. 13/17 via Eq. 4):  xi1' = M xi1 + K11 (lambda - rho h) + K12 b
-//      in fp64 (lane k < 22 owns row k of both channels);
+//      in fp64 (lane k < 22 owns row k; one channel per warp for T >= 2);
 //   B  c, s = P c_c, P c_s; theta = atan2(s, c); P^T theta (warp transpose-reduce);
 //   C  xi2 step (Eq. 19) and lambda_psi (Eq. 23b, G4) in fp64 (lanes k < 11);
 //   D  x, xdot, xddot, y, ..., psi at the lane's t (deviation from the boundary
@@ -26,6 +24,8 @@
 //      (Eq. 10-11):
 //        h_pos  = P^T (n R1 e - D) - Pd^T dv - Pdd^T da,
 //        h_copy = P^T ((n R2 + 1) e - E),      e = c - cos(psi)  (G9)
+//      with Pd = P Dm, Pdd = P Dm^2 (Dm: Bernstein derivative, tridiagonal),
+//      so D2 is one FP64 tensor-core product G = P^T [U0..U7];
 //   E  lambda <- lambda - rho h (Eq. 23a with F^T, G3).
 // The residual r1 = ||F xi1 - g|| is accumulated in the last iteration (or
 // every iteration in trace mode) from the same per-row quantities.
@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "bmc_internal.h"
 
@@ -170,6 +171,38 @@ __device__ __forceinline__ void mma_f64_884(double (&d)[2], double a, double b) 
                : "d"(a), "d"(b));
 }
 
+// atan2 for theta (Eq. 19): octant reduction and atan(a) = a + a^3 Q(a^2) on
+// [0, 1], Q of degree 8 from a weighted least-squares fit of the relative
+// error (2.6e-9 in exact arithmetic, so the fp32 result carries rounding only:
+// |error| < 7e-8 rad, unbiased -- a systematic fit error would add up
+// coherently in P^T theta).  pi/2 and pi enter as hi + lo pairs.
+// atan2(0, 0) = 0 (G18); signed zeros and the x < 0 half-plane follow atan2f.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mn * rcp_approx(mx);
+  const float s = a * a;
+  float p = -1.793621520e-03f;
+  p = fmaf(p, s, 1.091460537e-02f);
+  p = fmaf(p, s, -3.117784606e-02f);
+  p = fmaf(p, s, 5.795759474e-02f);
+  p = fmaf(p, s, -8.403450456e-02f);
+  p = fmaf(p, s, 1.095218584e-01f);
+  p = fmaf(p, s, -1.426424170e-01f);
+  p = fmaf(p, s, 1.999854829e-01f);
+  p = fmaf(p, s, -3.333329909e-01f);
+  float r = fmaf(a * s, p, a);
+  r = (ay > ax) ? (1.57079637f - r) + -4.37113883e-08f : r;
+  r = (x < 0.f) ? (3.14159274f - r) + -8.74227766e-08f : r;
+  r = copysignf(r, y);
+  return (mx == 0.f) ? 0.f : r;
+}
+
 // ------------------------------------------------------------ warp reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -271,7 +304,7 @@ struct Proj {
   const double* Pt64;    // the same basis in fp64 (contractions)
   const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
   const float4* abi;     // smem (a, b, a^2 or ab, kind) per obstacle
-  int q, n, ntf, rtail, rounds;
+  int q, n, rounds;
   bool all_circ;
   float nR1, nR2p1, v_max, a_max;
   float rlo, rhi;        // extent of the circle offsets along the heading
@@ -284,7 +317,7 @@ struct Proj {
 };
 
 // --------------------------------------------------- collision projections
-// For every obstacle j of the lane's group and circle i at sample t:
+// For every obstacle j and circle i at sample t:
 // x~ = X_i - x_j, y~ = Y_i - y_j (X_i = x + r_i cos psi, G9) and the
 // closed-form offset delta = (a d cos alpha, b d sin alpha) - (x~, y~) of
 // Eq. 21a / 22a:
@@ -298,9 +331,7 @@ struct Proj {
 // Circular obstacles: delta = 0 unless |(x~, y~)| < a, so blocks of JB
 // obstacles are first tested (x~, y~, |.|^2 only); a warp-wide OR of the
 // per-lane inside masks selects the obstacles whose closed form (rsqrt on
-// the MUFU pipe) must run.  In the split tail round lanes of different groups
-// visit different obstacles, so trip counts are made uniform with empty
-// slots.
+// the MUFU pipe) must run.
 //
 // The first pass tests the segment of circle centres {x + r u : r in
 // [rlo, rhi]}, u = (cos psi, sin psi), instead of each centre: with
@@ -487,7 +518,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
       c = fmaf(p[k], cc[k], c);
       s = fmaf(p[k], cs[k], s);
     }
-    const float tht = (c == 0.f && s == 0.f) ? 0.f : atan2f(s, c);
+    const float tht = atan2_fast(s, c);   // atan2(0, 0) = 0 (G18)
     ws->c[t] = c;
     ws->s[t] = s;
     ws->th[t] = tht;
@@ -514,17 +545,26 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
+  // D2: partial G = P^T U over this warp's own samples on the FP64 tensor
+  // cores (q x 11 basis, U = [U0 .. U7]: 11 x 8 outputs, all of them used):
+  // two m8n8k4 row tiles (basis rows 0..15, rows >= 11 clamped and
+  // discarded), k = 4 samples per step, issued right after each round's U so
+  // the MMAs overlap the next round's projections.  The Pdot / Pddot terms
+  // follow from G through Pdot^T u = Dm^T (P^T u) (see dm_apply), after the
+  // team sum.  fp64 products and sums: h -> 0 at a fixed point of the
+  // multipliers, so the sum over samples cancels and fp32 accumulation would
+  // dominate the error.  Each warp contracts the
+  // samples it projected itself, so no team barrier separates D1 from D2.
+  const double* __restrict__ P64 = pa.Pt64;
+  const int aoff0 = (lane >> 2) * QP64 + (lane & 3), aoff1 = min(8 + (lane >> 2), NV - 1) * QP64 + (lane & 3);
+  const float* __restrict__ ucol = &ws->U[lane >> 2][lane & 3];   // B fragment: U[k = lane % 4][n = lane / 4]
+  double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
 #pragma unroll 1
   for (int u = T - 1 - w; u < pa.rounds; u += T) {   // this warp's rounds (leader: the lightest)
-    int t, g, S, R;
-    if (u < pa.ntf) {
-      t = 32 * u + lane; g = 0; S = 1; R = 32;
-    } else {   // split tail round
-      R = pa.rtail; S = 32 / R;
-      t = 32 * pa.ntf + (lane & (R - 1)); g = lane / R;
-    }
-    const bool own = (g == 0);               // group 0 owns the sample's contributions
-    const bool valid = own && (t < q);
+    // samples t >= q of the last round have a zero basis row and far-away
+    // obstacle slots: they project to nothing and are excluded from the sums
+    const int t = 32 * u + lane;
+    const bool valid = t < q;
     // x = P c, xdot = Pdot c = P (Dm c), xddot = P (Dm^2 c): one basis row per k
     float x = 0.f, y = 0.f, xd = 0.f, yd = 0.f, xdd = 0.f, ydd = 0.f, psi = 0.f;
     {
@@ -566,12 +606,11 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     }
     float rc = 0.f;
     const float2* ob = pa.obs + t;
-    // circular obstacles in a full round: culled, blocked inside test
-    // (coll_circ); otherwise (ellipses, split tail round: few obstacles per
-    // lane) the plain loop.  A non-finite result (x~ = y~ = 0 exactly, G18,
-    // rare) reruns the plain loop with the guard; one call site keeps the
-    // hot loop small in the instruction cache.
-    bool general = !(pa.all_circ && S == 1);
+    // circular obstacles: culled, blocked inside test (coll_circ); ellipses:
+    // the plain loop.  A non-finite result (x~ = y~ = 0 exactly, G18, rare)
+    // reruns the plain loop with the guard; one call site keeps the hot loop
+    // small in the instruction cache.
+    bool general = !pa.all_circ;
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
       const float A = cull_tick(ws, u, t, x, y, psi, pa.rabs, lane);
@@ -589,7 +628,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     bool guard = false;
 #pragma unroll 1
     for (;;) {
-      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, g, S, X, Y, rec, res_s, Dx, Dy, rc);
+      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
       float chk = rc;
 #pragma unroll
       for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
@@ -600,14 +639,6 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       guard = true;
       general = true;
     }
-    for (int off = R; off < 32; off <<= 1) {   // combine obstacle groups (split tail round)
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        Dx[i] += __shfl_xor_sync(FULL, Dx[i], off);
-        Dy[i] += __shfl_xor_sync(FULL, Dy[i], off);
-      }
-      if (RES) rc += __shfl_xor_sync(FULL, rc, off);
-    }
     float Ds_x = 0.f, Ds_y = 0.f, Ex = 0.f, Ey = 0.f;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -616,7 +647,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       Ex = fmaf(r[i], Dx[i], Ex);
       Ey = fmaf(r[i], Dy[i], Ey);
     }
-    if (own) {
+    {
       ws->U[0][t] = fmaf(pa.nR1, ec, -Ds_x);
       ws->U[1][t] = fmaf(pa.nR2p1, ec, -Ex);
       ws->U[2][t] = fmaf(pa.nR1, es, -Ds_y);
@@ -631,37 +662,24 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       const float dth = ws->th[t] - psi;
       rps = fmaf(dth, dth, rps);
     }
+    __syncwarp();   // the round's U is complete
+    {
+      const int t0 = 32 * u;
+      const int ns = min(8, (q - t0 + 3) >> 2);
+#pragma unroll 4
+      for (int st = 0; st < ns; ++st) {
+        const int tt = t0 + 4 * st;
+        const double b = (double)ucol[tt];
+        mma_f64_884(g0, P64[aoff0 + tt], b);
+        mma_f64_884(g1, P64[aoff1 + tt], b);
+      }
+    }
   }
   __syncwarp();
   BMC_TICK(pc, 10);
-  // D2: partial G = P^T U over this warp's own samples on the FP64 tensor
-  // cores (q x 11 basis, U = [U0 .. U7]: 11 x 8 outputs, all of them used):
-  // two m8n8k4 row tiles (basis rows 0..15, rows >= 11 clamped and
-  // discarded), k = 4 samples per step.  The Pdot / Pddot terms follow from
-  // G through Pdot^T u = Dm^T (P^T u) (see dm_apply), after the team sum.
-  // fp64 products and sums: h -> 0 at a fixed point of the multipliers, so
-  // the sum over samples cancels and fp32 accumulation would dominate the
-  // error.  Each warp contracts the samples it
-  // projected itself, so no team barrier separates D1 from D2.
+  // C fragment: G[row g8 (+ 8)][column 2 c4 + i] -> partial slots [column][row]
   {
-    const double* __restrict__ P64 = pa.Pt64;
-    const int g8 = lane >> 2, c4 = lane & 3;   // fragment row / column group
-    const int aoff0 = g8 * QP64 + c4, aoff1 = min(8 + g8, NV - 1) * QP64 + c4;
-    const float* __restrict__ ucol = &ws->U[g8][c4];   // B fragment: U[k = c4][n = g8]
-    double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
-#pragma unroll 1
-    for (int u = T - 1 - w; u < pa.rounds; u += T) {
-      const int t0 = 32 * u;
-      const int ns = (u < pa.ntf) ? 8 : ((q - t0 + 3) >> 2);
-#pragma unroll 4
-      for (int st = 0; st < ns; ++st) {
-        const int t = t0 + 4 * st;
-        const double b = (double)ucol[t];
-        mma_f64_884(g0, P64[aoff0 + t], b);
-        mma_f64_884(g1, P64[aoff1 + t], b);
-      }
-    }
-    // C fragment: G[row g8 (+ 8)][column 2 c4 + i] -> partial slots [column][row]
+    const int g8 = lane >> 2, c4 = lane & 3;
     double* hp = pa.hp + w * HP_SLOTS;
     hp[(2 * c4) * 12 + g8] = g0[0];
     hp[(2 * c4 + 1) * 12 + g8] = g0[1];
@@ -806,14 +824,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.abi = abi;
   pa.q = q;
   pa.n = n;
-  pa.ntf = q / 32;
-  {
-    const int rem = q - 32 * pa.ntf;
-    int R = 1;
-    while (R < rem) R <<= 1;
-    pa.rtail = R;
-    pa.rounds = pa.ntf + (rem > 0 ? 1 : 0);
-  }
+  pa.rounds = (q + 31) / 32;
   pa.all_circ = all_circ;
   pa.nR1 = a.nR1;
   pa.nR2p1 = a.nR2p1;
@@ -1070,6 +1081,12 @@ cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
+#ifdef BMC_PROFILE
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M>) == cudaSuccess)
+      fprintf(stderr, "[bmc prof] kernel<%d>: %d regs, max %d threads/block, %zu B local\n", M, fa.numRegs,
+              fa.maxThreadsPerBlock, fa.localSizeBytes);
+#endif
   }
   const size_t smem = smem_bytes(a.n, ipc, a.team);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);

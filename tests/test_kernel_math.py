@@ -1,0 +1,92 @@
+"""Host-side checks of closed forms the CUDA kernel relies on (no GPU needed).
+
+* Bernstein derivative operator: Pdot = P Dm and Pddot = P Dm^2 with the tridiagonal
+  Dm of bmc_kernel.cuh (dm_apply), against the independent scipy basis of tests/helpers.
+* atan2_fast: the polynomial coefficients are parsed from bmc_kernel.cuh and evaluated
+  in float32 (numpy) exactly as the kernel orders the operations; error bound and bias
+  against numpy's arctan2 in fp64.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.helpers import bpoly_basis
+
+KERNEL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "paper_2109_13030_b200", "csrc", "bmc_kernel.cuh")
+
+
+def dm_matrix(n, T):
+    """(Dm c)_k = (-k c_{k-1} + (2k - n) c_k + (n - k) c_{k+1}) / T."""
+    D = np.zeros((n + 1, n + 1))
+    for k in range(n + 1):
+        if k >= 1:
+            D[k, k - 1] = -k / T
+        D[k, k] = (2 * k - n) / T
+        if k < n:
+            D[k, k + 1] = (n - k) / T
+    return D
+
+
+@pytest.mark.parametrize("q,T", [(100, 30.0), (50, 12.5), (128, 7.0), (33, 1.0)])
+def test_bernstein_derivative_operator(q, T):
+    P, Pd, Pdd = bpoly_basis(q, T, 10)
+    D = dm_matrix(10, T)
+    assert np.abs(P @ D - Pd).max() <= 1e-12 * np.abs(Pd).max()
+    assert np.abs(P @ D @ D - Pdd).max() <= 1e-12 * np.abs(Pdd).max()
+    # the transposed use in the contraction: Pd^T u = Dm^T (P^T u)
+    u = np.random.default_rng(0).standard_normal(q)
+    assert np.allclose(Pd.T @ u, D.T @ (P.T @ u), rtol=1e-12, atol=1e-12 * np.abs(Pd.T @ u).max())
+
+
+def _atan2_coeffs():
+    src = open(KERNEL).read()
+    body = src[src.index("float atan2_fast(float y, float x)"):]
+    body = body[:body.index("\n}\n")]
+    lead = float(re.search(r"float p = ([-0-9.e+]+)f;", body).group(1))
+    rest = [float(v) for v in re.findall(r"p = fmaf\(p, s, ([-0-9.e+]+)f\);", body)]
+    return [lead] + rest
+
+
+def atan2_fast_np(y, x):
+    f = np.float32
+    c = [f(v) for v in _atan2_coeffs()]
+    y = y.astype(f)
+    x = x.astype(f)
+    ax, ay = np.abs(x), np.abs(y)
+    mx, mn = np.maximum(ax, ay), np.minimum(ax, ay)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        a = (mn * (f(1) / mx)).astype(f)
+    s = (a * a).astype(f)
+    p = c[0]
+    for ck in c[1:]:
+        p = (p * s + ck).astype(f)          # fmaf: fp32 rounding of the fused result is closer still
+    r = ((a * s).astype(f) * p + a).astype(f)
+    r = np.where(ay > ax, ((f(1.57079637) - r).astype(f) + f(-4.37113883e-08)).astype(f), r)
+    r = np.where(x < 0, ((f(3.14159274) - r).astype(f) + f(-8.74227766e-08)).astype(f), r)
+    r = np.copysign(r, y)
+    return np.where(mx == 0, f(0), r)
+
+
+def test_atan2_fast_accuracy():
+    rng = np.random.default_rng(1)
+    ang = rng.uniform(-np.pi, np.pi, 400000)
+    rad = np.exp(rng.uniform(-6, 6, ang.size))
+    x, y = (rad * np.cos(ang)).astype(np.float32), (rad * np.sin(ang)).astype(np.float32)
+    got = atan2_fast_np(y, x).astype(np.float64)
+    ref = np.arctan2(y.astype(np.float64), x.astype(np.float64))
+    err = got - ref
+    assert np.abs(err).max() < 3e-7            # about 1 ulp of pi
+    assert abs(err.mean()) < 5e-9              # no systematic bias (it would add up in P^T theta)
+    small = np.abs(ref) < 1e-3                 # near the heading of a straight segment
+    assert np.max(np.abs(err[small]) / np.abs(ref[small])) < 3e-7
+
+
+def test_atan2_fast_special_cases():
+    z = np.float32(0)
+    assert atan2_fast_np(np.array([z]), np.array([z]))[0] == 0.0          # G18
+    assert atan2_fast_np(np.array([np.float32(0)]), np.array([np.float32(-1)]))[0] == np.float32(np.pi)
+    assert atan2_fast_np(np.array([np.float32(-0.0)]), np.array([np.float32(-1)]))[0] == -np.float32(np.pi)
+    assert atan2_fast_np(np.array([np.float32(1)]), np.array([np.float32(0)]))[0] == np.float32(np.pi / 2)
