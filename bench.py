@@ -163,7 +163,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="override instances per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=16)
-    ap.add_argument("--cpu-sample", type=int, default=48)
+    ap.add_argument("--cpu-sample", type=int, default=960,
+                    help="oracle instances for cpu_baseline (about 10-30 s on a 16-core host)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
