@@ -156,6 +156,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
   }
 }
 // MUFU.RSQ without the denormal fix-up sequence (x = 0 -> +inf).
+__device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT, ~1 ulp
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -344,12 +349,13 @@ struct Proj {
 // `build_active`); the pass records, per visited obstacle, the round's
 // clearance min_t |segment - o_j| - a_j stamped with the movement clock A.
 template <int M>
-__device__ __forceinline__ void coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
+__device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
                                           const int* __restrict__ list, int na, float* __restrict__ clr, float A,
                                           int lane, const float (&X)[M], const float (&Y)[M],
                                           float xc, float yc, float cu, float su, float rlo, float rhi,
                                           const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
                                           float (&Dy)[M], float& rc, long long* prof_need = nullptr) {
+  unsigned any_need = 0u;   // warp-uniform: some closed form ran
 #pragma unroll 1
   for (int jb = 0; jb < na; jb += JB) {
     unsigned mask = 0u, qm = 0u;
@@ -370,9 +376,10 @@ __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restri
     }
     if (lane < JB) {
       const int j = list[jb + lane];
-      clr[j] = sqrtf(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
+      clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
     }
     const unsigned need = __reduce_or_sync(FULL, mask);
+    any_need |= need;
 #ifdef BMC_PROFILE
     if (prof_need) *prof_need += __popc(need);
 #endif
@@ -398,6 +405,7 @@ __device__ __forceinline__ void coll_circ(const bool RES, const float2* __restri
       }
     }
   }
+  return any_need;
 }
 
 // Any obstacle kinds, one obstacle at a time.  GUARD handles x~ = y~ = 0
@@ -459,7 +467,7 @@ __device__ __forceinline__ float cull_tick(WarpSmem* ws, int u, int t, float x, 
   ws->prv[1][t] = y;
   ws->prv[2][t] = psi;
   // |.| of a NaN keeps a NaN bit pattern, which is above +inf: the clock becomes NaN
-  const float mv = fmaf(rabs, fabsf(dp), sqrtf(fmaf(dx, dx, dy * dy)));
+  const float mv = fmaf(rabs, fabsf(dp), sqrt_approx(fmaf(dx, dx, dy * dy)) * 1.000001f);
   const float mx = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(fabsf(mv))));
   const float A = ws->clk[u] + mx;
   __syncwarp();
@@ -600,9 +608,16 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       Y[i] = fmaf(r[i], sp, y);
       Dx[i] = 0.f;
       Dy[i] = 0.f;
-      rec[i] = r[i] * ec;
-      res_s[i] = r[i] * es;
-      base = fmaf(rec[i], rec[i], fmaf(res_s[i], res_s[i], base));
+      rec[i] = 0.f;
+      res_s[i] = 0.f;
+    }
+    if (RES) {   // residual-only terms
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        rec[i] = r[i] * ec;
+        res_s[i] = r[i] * es;
+        base = fmaf(rec[i], rec[i], fmaf(res_s[i], res_s[i], base));
+      }
     }
     float rc = 0.f;
     const float2* ob = pa.obs + t;
@@ -611,6 +626,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     // reruns the plain loop with the guard; one call site keeps the hot loop
     // small in the instruction cache.
     bool general = !pa.all_circ;
+    bool exact = general;   // warp-uniform: some closed form ran (only those can be non-finite)
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
       const float A = cull_tick(ws, u, t, x, y, psi, pa.rabs, lane);
@@ -622,8 +638,8 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
 #ifdef BMC_PROFILE
       pneed = &pc.acc[11];
 #endif
-      coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec, res_s,
-                   Dx, Dy, rc, pneed);
+      exact = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec,
+                           res_s, Dx, Dy, rc, pneed) != 0u;
     }
     bool guard = false;
 #pragma unroll 1
@@ -632,7 +648,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
       float chk = rc;
 #pragma unroll
       for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
-      if (guard || !__any_sync(FULL, !isfinite(chk))) break;
+      if (guard || !exact || !__any_sync(FULL, !isfinite(chk))) break;
 #pragma unroll
       for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
       rc = 0.f;
