@@ -306,6 +306,8 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   a.ref_dy = (has0 && hasT) ? pr->bnd[1][3] - pr->bnd[1][0] : 0.0;
   // development aid: BMC_PROF=1 with a PROFILE=1 build prints per-phase cycles
   const bool prof = std::getenv("BMC_PROF") != nullptr;
+  // testing aid: BMC_NOCULL=1 disables the exact culling (results must be bitwise equal)
+  if (const char* e = std::getenv("BMC_NOCULL")) a.no_cull = std::atoi(e) != 0;
   const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
   if (prof && cudaMalloc(&a.prof, sizeof(long long) * 12 * nwarps) == cudaSuccess)
     cudaMemsetAsync(a.prof, 0, sizeof(long long) * 12 * nwarps, s);

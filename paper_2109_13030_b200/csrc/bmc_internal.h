@@ -74,7 +74,8 @@ struct KernelArgs {
   // boundary line x_ref(t) = ref_x0 + ref_dx t/T (same for y): positions are
   // evaluated in fp32 as deviations from it
   double ref_x0, ref_dx, ref_y0, ref_dy;
-  long long* prof;             // [warps][10] phase cycles (PROFILE builds only) or null
+  long long* prof;             // [warps][12] phase cycles (PROFILE builds only) or null
+  int no_cull;                 // testing aid (BMC_NOCULL): every obstacle tested every round
 };
 
 struct SetupParams {

@@ -319,6 +319,7 @@ struct Proj {
   int npad, nclr;        // padded obstacle count (index npad = far dummy), stride
   double* hp;            // smem D2 partials of the team's warps, [T][HP_SLOTS]
   const double* dmtab;   // smem weights of Dm, Dm^T (dm_table)
+  bool no_cull;          // testing aid: test every obstacle (KernelArgs::no_cull)
 };
 
 // --------------------------------------------------- collision projections
@@ -630,7 +631,7 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
       const float A = cull_tick(ws, u, t, x, y, psi, pa.rabs, lane);
-      const int na = build_active(clr, pa.list, pa.npad, A, lane);
+      const int na = build_active(clr, pa.list, pa.npad, pa.no_cull ? INFINITY : A, lane);
 #ifdef BMC_PROFILE
       pc.acc[9] += na;
 #endif
@@ -859,6 +860,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.list = list_base + (size_t)warp * nclr;
   pa.hp = hp_base + (size_t)team * T * HP_SLOTS;
   pa.dmtab = ub + DM_TAB;
+  pa.no_cull = a.no_cull != 0;
   float r[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];

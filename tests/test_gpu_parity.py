@@ -245,3 +245,29 @@ def test_error_codes():
     big = np.zeros((161, 2, cfg.q), np.float32)
     with pytest.raises(BmcError):
         s.solve(_dev(pr["init"]), _dev(big), _dev(np.ones((161, 2), np.float32)), pr["bnd"], 3)
+
+
+@pytest.mark.parametrize("name,B", [("C1", 8), ("C3", 300), ("C4", 120)])
+def test_culling_is_exact(name, B, monkeypatch):
+    """The temporal culling of the inside test only skips obstacles whose contribution is
+    exactly zero: outputs are bitwise those of testing every obstacle (BMC_NOCULL=1)."""
+    cfg = CONFIGS[name]
+    pr = make_problem(cfg, 3, B=B)
+    s = _solver(cfg)
+    culled = run_gpu(cfg, pr, solver=s)
+    monkeypatch.setenv("BMC_NOCULL", "1")
+    full = run_gpu(cfg, pr, solver=s)
+    for k in culled:
+        assert np.array_equal(culled[k], full[k]), k
+
+
+@pytest.mark.parametrize("team", [1, 2, 4])
+def test_team_sizes_agree(team, monkeypatch):
+    """Any team size (warps per instance) gives the same answer up to summation order."""
+    cfg = CONFIGS["C3"]
+    pr = make_problem(cfg, 4, B=40)
+    ref = run_gpu(cfg, pr)
+    monkeypatch.setenv("BMC_TEAM", str(team))
+    g = run_gpu(cfg, pr)
+    compare(cfg, g, {k: ref[k].astype(np.float64) for k in ("coeffs", "cost", "residual")}, cfg.res_tol,
+            f"team {team}", check_best=False, oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr)
