@@ -147,6 +147,39 @@ def run_reference(args, cfg, rank, world):
 METRIC = "trajectories*iterations/s (batch solve: 1000 instances/GPU x 100 AM iterations)"
 
 
+def run_mpc(args, cfg):
+    """NEXT-1: MPC ticks (fresh STOMP samples, receding obstacles, warm-started lambda on the
+    device, one K = 10 solve, D2H of the best trajectory, host state update) per second."""
+    import torch
+    from paper_2109_13030_b200.mpc import MPC, GpuBackend, MPCConfig
+    from synth import make_tracks
+    torch.cuda.set_device(0)
+    mc = MPCConfig(cfg, horizon=10.0, dt=0.1, K=10, seed=0)
+    m = MPC(mc, make_tracks(cfg, 0), GpuBackend(mc), B=cfg.B)
+    for _ in range(args.warmup):
+        m.tick()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        m.tick()
+    wall = time.perf_counter() - t0
+    solve_ms = [r.solve_ms for r in m.log[args.warmup:]]
+    line = dict(metric=f"MPC control ticks/s (batch {cfg.B}, K = {mc.K} AM iterations per tick, horizon "
+                       f"{mc.horizon:g} s)", value=args.steps / wall, unit="ticks/s", n_gpus=1, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * wall / args.steps, higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f32 (fp64 KKT steps)", data="synthetic",
+                config={"workload": f"NEXT-1 MPC on the {cfg.name} scene: {cfg.n} dynamic obstacles, {cfg.m} circles, "
+                                    f"q = {cfg.q}, tick {mc.dt} s",
+                        "paper_budget_s_per_tick": 0.04},
+                solve_ms_per_tick={"mean": float(np.mean(solve_ms)), "max": float(np.max(solve_ms))},
+                gpu_launches=args.steps,
+                e2e={"value": args.steps / wall, "unit": "ticks/s",
+                     "h2d_bytes_per_step": int(cfg.B * 3 * 11 * 4 + cfg.n * 2 * cfg.q * 4 + cfg.n * 8),
+                     "d2h_bytes_per_step": int(55 * 4 + 8 + 4 + 8)},
+                robot={"t": m.t, "x": float(m.state[0, 0]), "y": float(m.state[1, 0])})
+    print(json.dumps(line), flush=True)
+
+
 def workload(cfg, world):
     return {"workload": f"{cfg.name}: batch {cfg.B}/GPU, horizon {cfg.q}, {cfg.m} circles, {cfg.n} "
                         f"{'dynamic' if cfg.dynamic else 'static'} obstacles, {cfg.K} AM iterations",
@@ -166,6 +199,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=960,
                     help="oracle instances for cpu_baseline (about 10-30 s on a 16-core host)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mpc", action="store_true",
+                    help="NEXT-1: time the receding-horizon MPC tick (P:585) instead of the C3 batch solve")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -178,6 +213,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
+        return
+    if args.mpc:
+        run_mpc(args, cfg)
         return
 
     import torch

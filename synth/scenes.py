@@ -145,6 +145,27 @@ def make_scene(cfg: Config, seed: int = 0, ab: Optional[np.ndarray] = None) -> d
     )
 
 
+def make_tracks(cfg: Config, seed: int = 0) -> dict:
+    """The obstacle motions of `make_scene` as constant-velocity tracks
+    (x0, y0, vx, vy [n] fp64, semi-axes ab [n][2]) for receding-horizon use."""
+    rng = np.random.default_rng(seed)
+    n = cfg.n
+    if n > 0:
+        x0, y0, vx, vy = (_dynamic_obstacles if cfg.dynamic else _static_obstacles)(rng, n)
+    else:
+        x0 = y0 = vx = vy = np.zeros(0)
+    return dict(x0=x0, y0=y0, vx=vx, vy=vy, ab=np.full((n, 2), CIRCLE_RADIUS + OBSTACLE_RADIUS))
+
+
+def tracks_at(tracks: dict, t0: float, q: int, T: float) -> np.ndarray:
+    """Obstacle positions obs_xy [n][2][q] fp32 at absolute times t0 + t_k."""
+    t = t0 + time_grid(q, T)
+    obs = np.empty((tracks["x0"].size, 2, q), dtype=np.float64)
+    obs[:, 0, :] = tracks["x0"][:, None] + tracks["vx"][:, None] * t[None, :]
+    obs[:, 1, :] = tracks["y0"][:, None] + tracks["vy"][:, None] * t[None, :]
+    return np.ascontiguousarray(obs.astype(np.float32))
+
+
 def line_control_points(bnd: np.ndarray = BND_STRAIGHT, degree: int = DEGREE) -> np.ndarray:
     """Control points [2][degree+1] of the constant-velocity segment start->goal."""
     s = np.arange(degree + 1) / degree
