@@ -87,6 +87,13 @@ def lib():
         L.or_lambda_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
         L.or_xi1_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
         L.or_xi2_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
+        L.or_philox4x32_10.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.or_philox4x32_10.restype = None
+        L.or_stomp_factor.argtypes = [C.c_int, _dp, C.POINTER(C.c_int)]
+        L.or_stomp_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_longlong, _dp]
+        L.or_stomp_normals.restype = None
+        L.or_sample_init.argtypes = [C.c_int, C.c_longlong, C.c_longlong, C.c_uint64, C.c_uint64, _dp,
+                                     C.c_double, C.c_double, C.c_int, _dp]
         _lib = L
     return _lib
 
@@ -284,3 +291,40 @@ class Oracle:
         out = np.zeros(self.nv)
         lib().or_xi2_step(self._h, _ptr(_f64(lampsi)), _ptr(_f64(theta)), _ptr(_f64(bnd)), _ptr(out))
         return out
+
+
+# ---- STOMP-style initial samples (sampler.c) -------------------------
+
+def philox4x32_10(ctr, key):
+    """One Philox4x32-10 block: 4 x uint32 counter, 2 x uint32 key -> 4 x uint32."""
+    c = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (C.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (C.c_uint32 * 4)()
+    lib().or_philox4x32_10(c, k, o)
+    return [int(v) for v in o]
+
+
+def stomp_factor(degree: int = 10) -> np.ndarray:
+    L = np.zeros(256)
+    nf = C.c_int(0)
+    rc = lib().or_stomp_factor(degree, _ptr(L), C.byref(nf))
+    if rc != 0:
+        raise ValueError(f"or_stomp_factor failed with code {rc}")
+    return L[: nf.value * nf.value].reshape(nf.value, nf.value)
+
+
+def stomp_normals(seed: int, stream: int, g: int) -> np.ndarray:
+    z = np.zeros(12)
+    lib().or_stomp_normals(seed, stream, g, _ptr(z))
+    return z
+
+
+def sample_init(B: int, bnd, seed: int, stream: int = 0, sigma_x: float = 1.0, sigma_y: float = 5.0,
+                index_base: int = 0, line_first: bool = True, degree: int = 10) -> np.ndarray:
+    """init [B][3][degree+1] fp64: straight segment p0 -> pT plus STOMP noise (reading G28)."""
+    out = np.zeros((B, 3, degree + 1))
+    rc = lib().or_sample_init(degree, B, index_base, seed, stream, _ptr(_f64(bnd)), sigma_x, sigma_y,
+                              int(line_first), _ptr(out))
+    if rc != 0:
+        raise ValueError(f"or_sample_init failed with code {rc}")
+    return out

@@ -112,6 +112,16 @@ int or_xi1_step(const or_ctx* c, const double* lam, const double* g,
 int or_xi2_step(const or_ctx* c, const double* lampsi, const double* theta,
                 const double* bnd, double* xi2_out);
 
+/* STOMP-style initial samples (sampler.c, reading G28).
+ * Philox4x32-10 block; the STOMP covariance factor (L [nf][nf] lower, nf = degree - 5);
+ * the 12 normals of instance g (10 used); init [B][3][nv] = line + noise. */
+#include <stdint.h>
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+int or_stomp_factor(int degree, double* L, int* nfree);
+void or_stomp_normals(uint64_t seed, uint64_t stream, long long g, double z[12]);
+int or_sample_init(int degree, long long B, long long index_base, uint64_t seed, uint64_t stream,
+                   const double* bnd, double sigma_x, double sigma_y, int line_first, double* init);
+
 #ifdef __cplusplus
 }
 #endif
