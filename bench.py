@@ -148,8 +148,9 @@ METRIC = "trajectories*iterations/s (batch solve: 1000 instances/GPU x 100 AM it
 
 
 def run_mpc(args, cfg):
-    """NEXT-1: MPC ticks (fresh STOMP samples, receding obstacles, warm-started lambda on the
-    device, one K = 10 solve, D2H of the best trajectory, host state update) per second."""
+    """NEXT-1: MPC ticks (fresh STOMP samples drawn on the device (NEXT-2), receding obstacles,
+    warm-started lambda on the device, one K = 10 solve, D2H of the best trajectory, host state
+    update) per second."""
     import torch
     from paper_2109_13030_b200.mpc import MPC, GpuBackend, MPCConfig
     from synth import make_tracks
@@ -172,9 +173,9 @@ def run_mpc(args, cfg):
                                     f"q = {cfg.q}, tick {mc.dt} s",
                         "paper_budget_s_per_tick": 0.04},
                 solve_ms_per_tick={"mean": float(np.mean(solve_ms)), "max": float(np.max(solve_ms))},
-                gpu_launches=args.steps,
+                gpu_launches=2 * args.steps,   # bmc_sample_init + bmc_solve per tick
                 e2e={"value": args.steps / wall, "unit": "ticks/s",
-                     "h2d_bytes_per_step": int(cfg.B * 3 * 11 * 4 + cfg.n * 2 * cfg.q * 4 + cfg.n * 8),
+                     "h2d_bytes_per_step": int(cfg.n * 2 * cfg.q * 4 + cfg.n * 8),   # samples drawn on the device
                      "d2h_bytes_per_step": int(55 * 4 + 8 + 4 + 8)},
                 robot={"t": m.t, "x": float(m.state[0, 0]), "y": float(m.state[1, 0])})
     print(json.dumps(line), flush=True)

@@ -138,6 +138,33 @@ int32_t bmc_pack_best(const int64_t* best, const float* coeffs, int64_t index_ba
 int32_t bmc_select_best(const int64_t* records, int32_t nranks, int64_t* best_out, float* coeffs_out,
                         bmc_stream_t stream);
 
+/* ---- STOMP-style initial samples on the device ---------
+ * "Our batch optimizer was always initialized with a Gaussian
+ * distribution proposed in [STOMP] centered around a straight-line
+ * trajectory."  Reading G28: init[l] = the constant-velocity
+ * segment from (bnd[0][0], bnd[1][0]) to (bnd[0][3], bnd[1][3]) as degree-10
+ * Bernstein control points (c_k = p0 + (pT - p0) k / 10), plus on the control
+ * points 3..7 (which enter no position, velocity or acceleration at either end)
+ * the STOMP smoothness noise s L z, L L^T = R^-1 / max diag(R^-1), R = D^T D
+ * with D the second difference of the control polygon restricted to those
+ * points; s = sigma_x for x, sigma_y for y; c_psi = 0.  z: 10 standard
+ * normals of global instance g = index_base + l from Philox4x32-10 (key =
+ * seed, counters (g, stream + j), j = 0..2) through Box-Muller in fp64 -- the
+ * same counter-based stream as the test oracle, so a sample depends only on
+ * (seed, stream, g), never on the batch split.  line_first: global instance 0
+ * is the unperturbed segment.  Output: device init [B][3][11] fp32
+ * (bmc_problem.init layout), caller-owned.  One kernel on `stream`.
+ * Errors: BMC_EINVAL (B < 0, init NULL with B > 0, non-finite bnd or sigma,
+ * degree != 10), BMC_ECUDA (launch failure). */
+typedef struct {
+  int64_t B, index_base;
+  uint64_t seed, stream;
+  double bnd[3][6];        /* x, y, psi x (p0, v0, a0, pT, vT, aT); p0 and pT of x, y are used */
+  double sigma_x, sigma_y; /* [m] */
+  int32_t line_first;
+} bmc_sample_params;
+int32_t bmc_sample_init(bmc_ctx* ctx, const bmc_sample_params* sp, float* init, bmc_stream_t stream);
+
 /* Kernel launches issued by the last bmc_solve / bmc_solve_host on ctx. */
 int32_t bmc_last_launch_count(const bmc_ctx* ctx);
 

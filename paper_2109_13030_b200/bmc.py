@@ -42,6 +42,12 @@ class BmcResult(C.Structure):
                 ("cost", C.c_void_p), ("res_trace", C.c_void_p), ("best", C.c_void_p)]
 
 
+class BmcSampleParams(C.Structure):
+    _fields_ = [("B", C.c_int64), ("index_base", C.c_int64), ("seed", C.c_uint64), ("stream", C.c_uint64),
+                ("bnd", C.c_double * 18), ("sigma_x", C.c_double), ("sigma_y", C.c_double),
+                ("line_first", C.c_int32)]
+
+
 class BmcError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"{_ERRNAMES.get(code, code)}: {msg}")
@@ -75,6 +81,8 @@ def load_library(path: str = LIBPATH):
         L.bmc_pack_best.restype = C.c_int32
         L.bmc_select_best.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.bmc_select_best.restype = C.c_int32
+        L.bmc_sample_init.argtypes = [C.c_void_p, C.POINTER(BmcSampleParams), C.c_void_p, C.c_void_p]
+        L.bmc_sample_init.restype = C.c_int32
         _lib = L
     return _lib
 
@@ -154,6 +162,22 @@ class Solver:
         L = load_library()
         _check(L.bmc_solve(self._h, C.byref(prob), C.byref(res), C.c_void_p(stream.cuda_stream)))
         self.last_launches = L.bmc_last_launch_count(self._h)
+        return out
+
+    def sample_init(self, B: int, bnd, seed: int, stream: int = 0, sigma_x: float = 1.0, sigma_y: float = 5.0,
+                    index_base: int = 0, line_first: bool = True, out=None, cuda_stream=None):
+        """STOMP-style initial samples on the device (bmc_sample_init): [B][3][11] fp32 tensor."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if out is None:
+            out = torch.empty((B, 3, NV), dtype=torch.float32, device=dev)
+        bnd = np.asarray(bnd, dtype=np.float64).reshape(18)
+        sp = BmcSampleParams(B, index_base, int(seed) & 0xFFFFFFFFFFFFFFFF, int(stream) & 0xFFFFFFFFFFFFFFFF,
+                             (C.c_double * 18)(*bnd), sigma_x, sigma_y, int(line_first))
+        if cuda_stream is None:
+            cuda_stream = torch.cuda.current_stream(dev)
+        _check(load_library().bmc_sample_init(self._h, C.byref(sp), C.c_void_p(_ptr(out)),
+                                              C.c_void_p(cuda_stream.cuda_stream)))
         return out
 
     def solve_host(self, init: np.ndarray, obs_xy: np.ndarray, obs_ab: np.ndarray, bnd, iters: int,

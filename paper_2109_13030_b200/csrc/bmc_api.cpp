@@ -75,11 +75,42 @@ struct bmc_ctx {
 
 extern "C" {
 
-int32_t bmc_version(void) { return 100; }
+int32_t bmc_version(void) { return 101; }
 
 const char* bmc_last_error(void) { return g_err.c_str(); }
 
 int32_t bmc_last_launch_count(const bmc_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+int32_t bmc_sample_init(bmc_ctx* ctx, const bmc_sample_params* sp, float* init, bmc_stream_t stream) {
+  if (!ctx) return fail(BMC_EINVAL, "ctx is NULL");
+  if (!sp) return fail(BMC_EINVAL, "sample params is NULL");
+  if (sp->B < 0) return fail(BMC_EINVAL, "B < 0");
+  if (sp->B > 0 && !init) return fail(BMC_EINVAL, "init is NULL");
+  if (ctx->p.degree != 10) return fail(BMC_EINVAL, "degree must be 10");
+  if (!std::isfinite(sp->sigma_x) || !std::isfinite(sp->sigma_y)) return fail(BMC_EINVAL, "non-finite sigma");
+  for (int ch = 0; ch < 2; ++ch)
+    if (!std::isfinite(sp->bnd[ch][0]) || !std::isfinite(sp->bnd[ch][3])) return fail(BMC_EINVAL, "non-finite bnd");
+  SampleArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.init = init;
+  a.B = sp->B;
+  a.index_base = sp->index_base;
+  a.seed = sp->seed;
+  a.stream = sp->stream;
+  a.x0 = sp->bnd[0][0];
+  a.xT = sp->bnd[0][3];
+  a.y0 = sp->bnd[1][0];
+  a.yT = sp->bnd[1][3];
+  a.sigma_x = sp->sigma_x;
+  a.sigma_y = sp->sigma_y;
+  a.line_first = sp->line_first != 0;
+  if (stomp_factor(a.L) != 0) return fail(BMC_ESINGULAR, "STOMP covariance factor");
+  DeviceGuard g(ctx->p.device);
+  cudaError_t e = launch_stomp(a, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "stomp_kernel launch");
+  g_err.clear();
+  return BMC_OK;
+}
 
 static int32_t validate_params(const bmc_params* p) {
   if (!p) return fail(BMC_EINVAL, "params is NULL");

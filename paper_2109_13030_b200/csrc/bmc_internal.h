@@ -1,6 +1,8 @@
 // bmc_internal.h -- shared between the host setup (setup.cpp), the C-ABI
 // (bmc_api.cpp) and the fused kernel (bmc_kernel.cu).  Product path only.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -86,6 +88,20 @@ struct SetupParams {
   double rho, rho_psi, w_copy;
   unsigned mask;
 };
+
+// STOMP sampler (bmc_sample.cu; contract in include/bmc.h bmc_sample_init)
+struct SampleArgs {
+  float* init;                 // [B][3][11]
+  long long B, index_base;
+  unsigned long long seed, stream;
+  double x0, xT, y0, yT;       // segment end points
+  double sigma_x, sigma_y;
+  double L[5][5];              // STOMP factor (lower), setup.cpp stomp_factor
+  int line_first;
+};
+cudaError_t launch_stomp(const SampleArgs& a, cudaStream_t s);
+// L L^T = R^-1 / max diag (R = D^T D on the control points 3..7 of degree 10)
+int stomp_factor(double L[5][5]);
 
 // host-side constants for one (params, n)
 struct HostConsts {

@@ -79,6 +79,40 @@ bool lu_inverse(std::vector<double> a, int N, std::vector<double>& inv) {
 
 }  // namespace
 
+// STOMP smoothness prior on the control points 3..7 of a degree-10 curve:
+// R = D^T D (D: second difference of the control polygon), Sigma = R^-1
+// normalised to unit maximum variance, L its Cholesky factor (G28).
+int stomp_factor(double L[5][5]) {
+  constexpr int nf = 5, f0 = 3;
+  std::vector<double> R(nf * nf), Rinv;
+  for (int a = 0; a < nf; ++a)
+    for (int b = 0; b < nf; ++b) {
+      double s = 0.0;
+      for (int i = 0; i < NV - 2; ++i) {   // rows of D: (1, -2, 1) at columns i .. i+2
+        auto d = [&](int k) { return k == i ? 1.0 : k == i + 1 ? -2.0 : k == i + 2 ? 1.0 : 0.0; };
+        s += d(f0 + a) * d(f0 + b);
+      }
+      R[a * nf + b] = s;
+    }
+  if (!lu_inverse(R, nf, Rinv)) return 2;
+  double dmax = 0.0;
+  for (int a = 0; a < nf; ++a) dmax = std::fmax(dmax, Rinv[a * nf + a]);
+  for (int a = 0; a < nf; ++a)
+    for (int b = 0; b < nf; ++b) L[a][b] = 0.0;
+  for (int i = 0; i < nf; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = Rinv[i * nf + j] / dmax;
+      for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
+      if (i == j) {
+        if (!(s > 0.0)) return 2;
+        L[i][i] = std::sqrt(s);
+      } else {
+        L[i][j] = s / L[j][j];
+      }
+    }
+  return 0;
+}
+
 int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err) {
   const int q = p.q, QP = Q_MAX, deg = NV - 1;  // fixed sample stride (compile-time in the kernel)
   out->q = q;

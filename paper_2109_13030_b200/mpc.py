@@ -11,7 +11,9 @@ size of 1000."  Every control tick:
      v_des along +x), x = v_des (t_now + T_h), y = 0, zero heading and rates;
   2. samples: fresh STOMP-style Gaussian samples around the straight segment
      start -> goal ("always initialized with a Gaussian distribution
-     ... centered around a straight-line trajectory", synth.make_init);
+     ... centered around a straight-line trajectory"), drawn by the backend:
+     bmc_sample_init on the device (NEXT-2: Philox stream (seed, tick)), the
+     oracle sampler in the tests, synth.make_init for a backend without one;
   3. one batch solve of K iterations with lambda_in = the previous tick's
      lambda_out, instance by instance (kept on the device);
   4. execute dt of the best trajectory (argmin key, G17): the new state is the
@@ -101,10 +103,14 @@ class MPC:
         return bnd
 
     def problem(self) -> dict:
-        sc = self.mc.solve_cfg
+        sc, mc = self.mc.solve_cfg, self.mc
         bnd = self.boundary()
-        init = make_init(sc, seed=self.mc.seed * 100003 + self.tick_no, B=self.B,
-                         sigma_x=self.mc.sigma_x, sigma_y=self.mc.sigma_y, bnd=bnd)
+        if hasattr(self.backend, "sample"):
+            init = self.backend.sample(self.B, bnd, seed=mc.seed, stream=self.tick_no, sigma_x=mc.sigma_x,
+                                       sigma_y=mc.sigma_y)
+        else:
+            init = make_init(sc, seed=mc.seed * 100003 + self.tick_no, B=self.B, sigma_x=mc.sigma_x,
+                             sigma_y=mc.sigma_y, bnd=bnd)
         obs = tracks_at(self.tracks, self.t, sc.q, sc.T)
         ab = np.ascontiguousarray(self.tracks["ab"].astype(np.float32))
         return dict(init=init, obs_xy=obs, obs_ab=ab, bnd=bnd)
@@ -141,9 +147,18 @@ class GpuBackend:
         self.out = None
         self.ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
 
+    def sample(self, B, bnd, seed, stream, sigma_x, sigma_y):
+        """STOMP samples drawn on the device (bmc_sample_init, NEXT-2); stays on the device."""
+        buf = getattr(self, "init_buf", None)
+        if buf is not None and buf.shape[0] != B:
+            buf = None
+        self.init_buf = self.solver.sample_init(B, bnd, seed, stream, sigma_x=sigma_x, sigma_y=sigma_y, out=buf)
+        return self.init_buf
+
     def __call__(self, init, obs_xy, obs_ab, bnd, K, lam):
         torch = self.torch
-        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, non_blocking=True)
+        d = lambda a: a if isinstance(a, torch.Tensor) else \
+            torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, non_blocking=True)
         init_d, obs_d, ab_d = d(init), d(obs_xy), d(obs_ab)
         B = init.shape[0]
         if self.out is None or self.out[0]["coeffs"].shape[0] != B:

@@ -5,6 +5,7 @@ evaluation helper against scipy."""
 import numpy as np
 import pytest
 
+import oracle
 from oracle import Oracle
 from paper_2109_13030_b200.mpc import MPC, MPCConfig, bernstein_rows
 from synth import CONFIGS, make_tracks
@@ -27,6 +28,9 @@ class OracleBackend:
     def __init__(self, cfg):
         self.o = Oracle(oracle_params(cfg), cfg.n)
         self.calls = []
+
+    def sample(self, B, bnd, seed, stream, sigma_x, sigma_y):   # the oracle's STOMP sampler (NEXT-2)
+        return oracle.sample_init(B, bnd, seed, stream, sigma_x=sigma_x, sigma_y=sigma_y).astype(np.float32)
 
     def __call__(self, init, obs_xy, obs_ab, bnd, K, lam):
         out = self.o.solve(bnd, obs_xy, obs_ab, init, K, lambda_in=lam)
