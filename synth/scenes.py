@@ -166,6 +166,34 @@ def tracks_at(tracks: dict, t0: float, q: int, T: float) -> np.ndarray:
     return np.ascontiguousarray(obs.astype(np.float32))
 
 
+def scene_blocker(q: int = 100, x: float = 15.0, a: float = 1.5) -> dict:
+    """NEXT-3 (Fig. 1c): one static obstacle of semi-axes a on the straight
+    start -> goal line; the batch should find both homotopy classes (above / below)."""
+    obs = np.zeros((1, 2, q))
+    obs[0, 0, :] = x
+    return dict(obs_xy=obs.astype(np.float32), obs_ab=np.full((1, 2), a, np.float32), bnd=BND_STRAIGHT.copy())
+
+
+def scene_wall_gap(q: int = 100, x: float = 15.0, gap: float = 1.2, half_width: float = 3.6,
+                   human: float = OBSTACLE_RADIUS, inflate: float = CIRCLE_RADIUS) -> dict:
+    """NEXT-3 (Table II trend): a wall of humans (radius `human`, centre spacing
+    2 human) across the line at x, with a free gap of width `gap` centred on y = 0.  Obstacles
+    are inflated by `inflate` (the footprint circle radius: 0.3 m for the multi-circle robot,
+    0.8 m for the single disk that covers the same 1.6 x 0.6 m footprint)."""
+    edge = gap / 2 + human
+    ys = []
+    y = edge
+    while y <= half_width:
+        ys += [y, -y]
+        y += 2 * human
+    n = len(ys)
+    obs = np.zeros((n, 2, q))
+    obs[:, 0, :] = x
+    obs[:, 1, :] = np.array(ys)[:, None]
+    return dict(obs_xy=obs.astype(np.float32), obs_ab=np.full((n, 2), human + inflate, np.float32),
+                bnd=BND_STRAIGHT.copy())
+
+
 def line_control_points(bnd: np.ndarray = BND_STRAIGHT, degree: int = DEGREE) -> np.ndarray:
     """Control points [2][degree+1] of the constant-velocity segment start->goal."""
     s = np.arange(degree + 1) / degree
