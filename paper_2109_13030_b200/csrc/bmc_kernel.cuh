@@ -43,7 +43,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int QP = Q_MAX;   // sample stride of every per-sample smem array
-constexpr int JB = 8;       // obstacles per inside-test block
+constexpr int JB = 4;       // obstacles per inside-test block
 
 constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per round
 constexpr int QP64 = QP + 4;     // row stride of the fp64 basis (BlobLayout::p64_stride)
@@ -364,13 +364,13 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
     for (int jj = 0; jj < JB; ++jj) {
       const int j = list[jb + jj];   // the list is padded to a multiple of JB with a far dummy
       const float2 o = ob[j * QP];
-      const float a2 = abi[j].z;
+      const float thr = abi[j].z;   // a^2 (1 + 1e-5) + 1e-5
       const float dx = xc - o.x, dy = yc - o.y;
       const float d0 = fmaf(dy, dy, dx * dx), bd = fmaf(dy, su, dx * cu);
       const float rs = fmaxf(rlo, fminf(rhi, -bd));
       const float qmin = fmaf(rs, fmaf(2.f, bd, rs), d0);
       // margin: absolute rounding of qmin is < 1e-6 m^2 for any obstacle within reach
-      mask |= (qmin < fmaf(a2, 1.00001f, 1e-5f)) ? (1u << jj) : 0u;
+      mask |= (qmin < thr) ? (1u << jj) : 0u;
       // round minimum of qmin (non-negative floats order as their bit patterns)
       const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(fmaxf(qmin, 0.f)));
       qm = (lane == jj) ? mn : qm;
@@ -804,7 +804,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
-    abi[j] = make_float4(aa, bb, kind == 0.f ? aa * aa : aa * bb, kind);
+    // z: circles -> the inside-test threshold a^2 (1 + 1e-5) + 1e-5 m^2 (coll_circ; covers
+    // the fp32 rounding of the segment distance), ellipses -> a b (scaled rule)
+    abi[j] = make_float4(aa, bb, kind == 0.f ? fmaf(aa * aa, 1.00001f, 1e-5f) : aa * bb, kind);
     circ &= (aa == bb);
   }
   for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
