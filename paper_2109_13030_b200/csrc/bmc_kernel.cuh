@@ -156,6 +156,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
   }
 }
 // MUFU.RSQ without the denormal fix-up sequence (x = 0 -> +inf).
+// fp32 -> fp64 without the -ftz denormal flush (a flush would cost an extra FMUL)
+__device__ __forceinline__ double f2d(float x) {
+  double d;
+  asm("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(x));
+  return d;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT, ~1 ulp
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -531,7 +537,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     ws->c[t] = c;
     ws->s[t] = s;
     ws->th[t] = tht;
-    const double thd = (double)tht;
+    const double thd = f2d(tht);
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
   }
@@ -682,13 +688,24 @@ __device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, co
     __syncwarp();   // the round's U is complete
     {
       const int t0 = 32 * u;
-      const int ns = min(8, (q - t0 + 3) >> 2);
-#pragma unroll 4
-      for (int st = 0; st < ns; ++st) {
-        const int tt = t0 + 4 * st;
-        const double b = (double)ucol[tt];
-        mma_f64_884(g0, P64[aoff0 + tt], b);
-        mma_f64_884(g1, P64[aoff1 + tt], b);
+      const float* __restrict__ up = ucol + t0;
+      const double* __restrict__ a0 = P64 + aoff0 + t0;
+      const double* __restrict__ a1 = P64 + aoff1 + t0;
+      if (t0 + 32 <= q) {   // full round: 8 steps, immediate offsets
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {
+          const double b = f2d(up[4 * st]);
+          mma_f64_884(g0, a0[4 * st], b);
+          mma_f64_884(g1, a1[4 * st], b);
+        }
+      } else {
+        const int ns = (q - t0 + 3) >> 2;
+#pragma unroll 1
+        for (int st = 0; st < ns; ++st) {
+          const double b = f2d(up[4 * st]);
+          mma_f64_884(g0, a0[4 * st], b);
+          mma_f64_884(g1, a1[4 * st], b);
+        }
       }
     }
   }
