@@ -554,8 +554,8 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 //   U0 = n R1 e_c - D_x, U1 = (n R2 + 1) e_c - E_x, U2, U3 likewise for y,
 //   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
-template <int M>
-__device__ __forceinline__ void phase_project(const bool RES, const Proj& pa, const float (&r)[M], WarpSmem* ws,
+template <int M, bool RES>
+__device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
                                               int lane, int w, int T, int team, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
@@ -1008,7 +1008,12 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       BMC_TICK(pc, 4);
       // ---- D: projections (own rounds) + contraction (owned channels) ---------
       const bool want_res = trace ? (it >= 0) : (it == K - 1);
-      phase_project<M>(want_res, pa, r, ws, lane, w, T, team, pc);
+      // residual terms only where they are reported: a compile-time flag keeps the
+      // hot (RES = false) copy free of the per-round re-evaluation of a runtime flag
+      if (want_res)
+        phase_project<M, true>(pa, r, ws, lane, w, T, team, pc);
+      else
+        phase_project<M, false>(pa, r, ws, lane, w, T, team, pc);
       __syncwarp();
       BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
