@@ -770,7 +770,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #else
 #define BMC_KERNEL_BOUNDS __launch_bounds__(512)
 #endif
-template <int M>
+template <int M, int TT>
 __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
@@ -783,7 +783,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   float4* abi = reinterpret_cast<float4*>(obs + (size_t)(npad + 1) * QP);
   double* ub = reinterpret_cast<double*>(abi + npad + 1);
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
-  const int T = a.team, ipc = wpc / T;               // warps per instance, instances per CTA
+  constexpr int T = TT;                              // warps per instance (compile time: folds the
+  const int ipc = wpc / T;                           // team bookkeeping), instances per CTA
   const int team = warp / T, w = warp - team * T;    // instance slot in the CTA, rank in the team
   float* clr_base = reinterpret_cast<float*>(wsbase + ipc);
   int* list_base = reinterpret_cast<int*>(clr_base + (size_t)ipc * T_MAX * nclr);
@@ -1113,27 +1114,38 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 
 size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 
-// One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
-// this; bmc_launch.cu dispatches on m.
-template <int M>
-cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
+// Launch of one (M, team size) kernel variant.
+template <int M, int TT>
+cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done = true;
 #ifdef BMC_PROFILE
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M>) == cudaSuccess)
-      fprintf(stderr, "[bmc prof] kernel<%d>: %d regs, max %d threads/block, %zu B local\n", M, fa.numRegs,
+    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT>) == cudaSuccess)
+      fprintf(stderr, "[bmc prof] kernel<%d,%d>: %d regs, max %d threads/block, %zu B local\n", M, TT, fa.numRegs,
               fa.maxThreadsPerBlock, fa.localSizeBytes);
 #endif
   }
-  const size_t smem = smem_bytes(a.n, ipc, a.team);
+  const size_t smem = smem_bytes(a.n, ipc, TT);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
-  bmc_am_kernel<M><<<grid, 32 * a.team * ipc, smem, s>>>(a);
+  bmc_am_kernel<M, TT><<<grid, 32 * TT * ipc, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
+// this; bmc_launch.cu dispatches on m.  Team sizes 1, 2, 4.
+template <int M>
+cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
+  switch (a.team) {
+    case 1: return launch_am_mt<M, 1>(a, ipc, s);
+    case 2: return launch_am_mt<M, 2>(a, ipc, s);
+    case 4: return launch_am_mt<M, 4>(a, ipc, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace bmc
