@@ -914,6 +914,18 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
     double xi2r = (k < NV) ? (double)ini[2 * NV + k] : 0.0;
     double lamp = (li && k < NV) ? (double)li[2 * NV2 + k] : 0.0;
+    // lambda_psi step of Eq. 23b, deferred from phase C to the next phase A (where it
+    // overlaps the xi1 mat-vec): lamp <- lamp - (rho_psi P^T P xi2 - rho_psi P^T theta)
+    double pth_prev = 0.0;
+    bool lp_pending = false;
+    auto lampsi_step = [&]() {
+      const int k1 = min(k, NV - 1);
+      double g4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
+      const double v = lamp - (((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth_prev);
+      lamp = (k < NV) ? v : 0.0;
+    };
     if (k < NV) { ws->cf4[w][k] = (float)xi2r; ws->xi2w[w][k] = xi2r; }
 
     float r1sq = 0.f, rpsq = 0.f;
@@ -938,6 +950,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           const int kc = min(k, NV2 - 1);
           if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * ws->h[ch][k];
           __syncwarp();
+          if (c == 0 && lp_pending) lampsi_step();
           {
             // 8 independent fp64 chains (depth <= 6): the step is latency-bound
             double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -967,6 +980,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
         }
         if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
+      if (nown == 0 && lp_pending) lampsi_step();   // warps without a channel (T = 4)
+      lp_pending = false;
       BMC_TICK(pc, 0);
       team_sync(team, T);
       BMC_TICK(pc, 1);
@@ -996,14 +1011,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
             ws->cf4[w][k] = (float)xi2r;
           }
         }
-        __syncwarp();
-        {
-          double g4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-          for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
-          const double v = lamp - (((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth);
-          lamp = (k < NV) ? v : 0.0;
-        }
+        pth_prev = pth;        // the lambda_psi step runs in the next phase A
+        lp_pending = true;
       }
       __syncwarp();
       BMC_TICK(pc, 4);
@@ -1040,6 +1049,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     if (lane == 0 && a.prof)
       for (int i = 0; i < 12; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * 12 + i] = pc.acc[i];
 #endif
+    __syncwarp();
+    if (lp_pending) lampsi_step();   // the last iteration's lambda_psi step
     // ---- outputs ----------------------------------------------------------------
     if (active) {
       float* co = a.coeffs + l * 5 * NV;
