@@ -21,7 +21,7 @@ def load(dis_path, csv_path):
     insts, in_k, cur = [], False, ('?', 0)
     for l in dis:
         if l.strip().startswith('.section') and '.text.' in l:
-            in_k = 'bmc_am_kernel' in l
+            in_k = os.environ.get('KSEL', 'bmc_am_kernel') in l
             continue
         if not in_k:
             continue
