@@ -176,6 +176,8 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 // FP64 tensor-core MMA D = A B + D, m8n8k4 (A row-major 8x4, B col-major 4x8):
 // a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
 // d[i] = D[lane / 4][2 (lane % 4) + i].
+// Operands must not come from lane-dependent selects: the compiler may split the
+// mma.sync into predicated copies, which deadlocks the warp (tests/test_sass.py).
 __device__ __forceinline__ void mma_f64_884(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
