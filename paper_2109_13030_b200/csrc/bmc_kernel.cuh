@@ -216,6 +216,30 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
   return (mx == 0.f) ? 0.f : r;
 }
 
+// sin and cos of the heading (G9) without the Payne-Hanek path of sincosf:
+// j = rint(x 2/pi), Cody-Waite reduction r = x - j pi/2 with a three-part pi/2
+// (P1 has 8 significant bits, so j P1 is exact for |j| < 2^16), and the
+// classic single-precision minimax polynomials on [-pi/4, pi/4] (Cephes sinf /
+// cosf); |error| < 1e-7 for |x| < 1e3 rad, unbiased (tests/test_kernel_math.py).
+// Headings beyond 1e5 rad only occur in diverged instances.
+__device__ __forceinline__ void sincos_fast(float x, float* sp, float* cp) {
+  const float j = rintf(x * 0.636619772367581343f);
+  float r = fmaf(j, -1.5703125f, x);
+  r = fmaf(j, -4.83751296997070312e-4f, r);
+  r = fmaf(j, -7.54978995489188216e-8f, r);
+  const float r2 = r * r;
+  float ps = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+  ps = fmaf(r2, ps, -1.6666654611e-1f);
+  const float sn = fmaf(r * r2, ps, r);
+  float pc = fmaf(r2, 2.443315711e-5f, -1.388731625e-3f);
+  pc = fmaf(r2, pc, 4.166664568e-2f);
+  const float cs = fmaf(r2 * r2, pc, fmaf(-0.5f, r2, 1.f));
+  const int q = (int)j;
+  const float s1 = (q & 1) ? cs : sn, c1 = (q & 1) ? sn : cs;
+  *sp = (q & 2) ? -s1 : s1;
+  *cp = ((q + 1) & 2) ? -c1 : c1;
+}
+
 // ------------------------------------------------------------ warp reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -491,6 +515,12 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
                                             float A, int lane) {
   int na = 0;
   const float lim = A + CULL_MARGIN;
+  if (npad <= 32) {   // the common case: one ballot
+    const bool act = (lane < npad) && !(clr[lane] > lim);
+    const unsigned bal = __ballot_sync(FULL, act);
+    if (act) list[__popc(bal & ((1u << lane) - 1u))] = lane;
+    na = __popc(bal);
+  } else {
 #pragma unroll 1
   for (int j0 = 0; j0 < npad; j0 += 32) {
     const int j = j0 + lane;
@@ -498,6 +528,7 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
     const unsigned bal = __ballot_sync(FULL, act);
     if (act) list[na + __popc(bal & ((1u << lane) - 1u))] = j;
     na += __popc(bal);
+  }
   }
   const int nap = (na + JB - 1) & ~(JB - 1);
   if (lane < nap - na) list[na + lane] = npad;
@@ -607,7 +638,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
     if (RES && valid) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
     float sp, cps;
-    sincosf(psi, &sp, &cps);
+    sincos_fast(psi, &sp, &cps);
     const float ec = ws->c[t] - cps, es = ws->s[t] - sp;
     float X[M], Y[M], Dx[M], Dy[M], rec[M], res_s[M];
     float base = 0.f;

@@ -262,12 +262,9 @@ def test_culling_is_exact(name, B, monkeypatch):
 
 
 @pytest.mark.parametrize("team", [1, 2, 4])
-def test_team_sizes_agree(team, monkeypatch):
-    """Any team size (warps per instance) gives the same answer up to summation order."""
+def test_team_sizes_meet_the_bar(team, monkeypatch):
+    """Every team size (warps per instance; summation orders differ) meets the parity bar."""
     cfg = CONFIGS["C3"]
     pr = make_problem(cfg, 4, B=40)
-    ref = run_gpu(cfg, pr)
     monkeypatch.setenv("BMC_TEAM", str(team))
-    g = run_gpu(cfg, pr)
-    compare(cfg, g, {k: ref[k].astype(np.float64) for k in ("coeffs", "cost", "residual")}, cfg.res_tol,
-            f"team {team}", check_best=False, oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr)
+    check(cfg, pr, f"C3 B=40 team {team}")

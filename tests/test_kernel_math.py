@@ -90,3 +90,40 @@ def test_atan2_fast_special_cases():
     assert atan2_fast_np(np.array([np.float32(0)]), np.array([np.float32(-1)]))[0] == np.float32(np.pi)
     assert atan2_fast_np(np.array([np.float32(-0.0)]), np.array([np.float32(-1)]))[0] == -np.float32(np.pi)
     assert atan2_fast_np(np.array([np.float32(1)]), np.array([np.float32(0)]))[0] == np.float32(np.pi / 2)
+
+
+def _sincos_consts():
+    src = open(KERNEL).read()
+    body = src[src.index("void sincos_fast(float x, float* sp, float* cp)"):]
+    body = body[:body.index("\n}\n")]
+    return [float(v) for v in re.findall(r"([-]?\d\.\d+e[-+]?\d+|[-]?\d\.\d{6,})f", body)]
+
+
+def sincos_fast_np(x):
+    """The kernel's sincos_fast in float32 numpy, constants parsed from the source in order:
+    2/pi, P1, P2, P3, S3, S2, S1, C3, C2, C1."""
+    f = np.float32
+    k = [f(v) for v in _sincos_consts()]
+    two_pi_inv, P1, P2, P3, S3, S2, S1, C3, C2, C1 = k
+    x = x.astype(f)
+    j = np.rint((x * two_pi_inv).astype(f)).astype(f)
+    r = (x - j * abs(P1)).astype(f)
+    r = (r - j * abs(P2)).astype(f)
+    r = (r - j * abs(P3)).astype(f)
+    r2 = (r * r).astype(f)
+    sn = (r + (r * r2).astype(f) * ((S1 + r2 * ((S2 + r2 * S3).astype(f))).astype(f))).astype(f)
+    cs = (f(1) - f(0.5) * r2 + (r2 * r2).astype(f) * ((C1 + r2 * ((C2 + r2 * C3).astype(f))).astype(f))).astype(f)
+    q = j.astype(np.int64)
+    s1, c1 = np.where(q & 1, cs, sn), np.where(q & 1, sn, cs)
+    return np.where(q & 2, -s1, s1), np.where((q + 1) & 2, -c1, c1)
+
+
+def test_sincos_fast_accuracy():
+    assert len(_sincos_consts()) == 10
+    x = np.concatenate([np.linspace(-50.0, 50.0, 400001),
+                        np.random.default_rng(2).uniform(-1e3, 1e3, 100000)]).astype(np.float32)
+    s, c = sincos_fast_np(x)
+    xs = x.astype(np.float64)
+    es, ec = s - np.sin(xs), c - np.cos(xs)
+    assert np.abs(es).max() < 1.5e-7 and np.abs(ec).max() < 1.5e-7
+    assert abs(es.mean()) < 1e-9 and abs(ec.mean()) < 1e-9

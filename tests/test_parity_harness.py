@@ -47,3 +47,33 @@ def test_accepts_perturbed_oracle_on_ill_conditioned_instance(c2):
     st = compare(cfg, g, ref, cfg.res_tol, "perturbed oracle", check_best=False, oracle=o, problem=pr)
     ill = {d["inst"] for d in st["ill_conditioned"]}
     assert ill <= {7, 15, 36} and len(ill) >= 1
+
+
+@pytest.fixture(scope="module")
+def c3_sensitive():
+    """C3 (seed 4) instances 2 and 8: #2 is infeasible (r1 ~ 1.15) and moves by ~1e-4 m /
+    5e-5 relative cost when obstacle positions move by 1e-6 m (the fp32 rounding of the
+    kernel's deviation frame); #8 barely moves."""
+    cfg = CONFIGS["C3"]
+    pr = make_problem(cfg, 4, B=40)
+    sub = dict(pr, init=np.ascontiguousarray(pr["init"][[2, 8]]))
+    o = Oracle(oracle_params(cfg), cfg.n)
+    ref = o.solve(sub["bnd"], sub["obs_xy"], sub["obs_ab"], sub["init"], cfg.K)
+    return cfg, sub, o, ref
+
+
+def test_obstacle_rounding_counts_as_intrinsic_spread(c3_sensitive):
+    cfg, pr, o, ref = c3_sensitive
+    g = {k: np.array(ref[k], copy=True) for k in ("coeffs", "cost", "residual")}
+    g["cost"][0] *= 1 + 2e-4        # what one GPU summation order gave on #2
+    st = compare(cfg, g, ref, cfg.res_tol, "sensitive", check_best=False, oracle=o, problem=pr)
+    assert [d["inst"] for d in st["ill_conditioned"]] == [0]
+
+
+def test_deviation_far_beyond_the_spread_is_rejected(c3_sensitive):
+    cfg, pr, o, ref = c3_sensitive
+    for inst, rel in ((0, 5e-3), (1, 3e-4)):
+        g = {k: np.array(ref[k], copy=True) for k in ("coeffs", "cost", "residual")}
+        g["cost"][inst] *= 1 + rel
+        with pytest.raises(AssertionError):
+            compare(cfg, g, ref, cfg.res_tol, "far", check_best=False, oracle=o, problem=pr)
