@@ -111,6 +111,18 @@ def test_c3_full_batch_sampled_instances():
         assert feas[bi] and g["cost"][bi] == g["cost"][feas].min()
 
 
+def test_c3_full_batch_every_instance():
+    """The bench launch (C3: B = 1000, K = 100), seed 4: every instance and the best index vs
+    the oracle (about 15 s of oracle time on 16 cores)."""
+    cfg = CONFIGS["C3"]
+    pr = make_problem(cfg, 4)
+    g = run_gpu(cfg, pr)
+    r = run_oracle(cfg, pr)
+    st = compare(cfg, g, r, cfg.res_tol, "C3 B=1000 all", oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr)
+    print(st)
+    assert len(st["ill_conditioned"]) <= 10      # about 0.5 % (DESIGN.md "Conditioning")
+
+
 def test_c4_full_batch_sampled_instances():
     """C4 (B = 1000, 4 circles, 50 obstacles, tight bounds, K = 200): 12 sampled instances."""
     cfg = CONFIGS["C4"]
