@@ -49,6 +49,10 @@ constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per
 constexpr int QP64 = QP + 4;     // row stride of the fp64 basis (BlobLayout::p64_stride)
 constexpr int QPU = QP + 4;      // row stride of WarpSmem::U
 constexpr int HP_SLOTS = 8 * 12; // per-warp partial contractions (D2), doubles
+#ifndef BMC_HANDOFF_STEPS
+#define BMC_HANDOFF_STEPS 8
+#endif
+constexpr int HANDOFF_STEPS = BMC_HANDOFF_STEPS;   // MMA steps of round 0 that warp 0 takes (T = 2)
 
 // Per-instance state shared by the T warps of its team.  The x and y channels
 // of xi1 are decoupled in the xi1 step and the lambda step (Eq. 10: F and the
@@ -116,13 +120,13 @@ __host__ __device__ inline int clr_stride(int n) { return pad_obstacles(n) + JB;
 // Layout after the constant blob: obstacles [npad + 1][QP] (row npad: the far
 // dummy), abi [npad + 1], u = K12 b, WarpSmem[ipc], clearance stamps
 // [ipc][4][nclr], active lists [ipc * T][nclr], D2 partials [ipc * T][HP_SLOTS],
-// mbarrier.
+// mbarriers (blob copy; one per team for the round-0 hand-off).
 __host__ __device__ inline size_t smem_bytes(int n, int ipc, int T) {
   const int np = pad_obstacles(n) + 1;
   return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
          U_DOUBLES * sizeof(double) + (size_t)ipc * sizeof(WarpSmem) +
          (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) + (size_t)ipc * T * HP_SLOTS * sizeof(double) +
-         16;
+         16 + (size_t)ipc * 8;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -144,6 +148,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {   // release, CTA scope
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
   unsigned done = 0;
@@ -352,6 +359,8 @@ struct Proj {
   double* hp;            // smem D2 partials of the team's warps, [T][HP_SLOTS]
   const double* dmtab;   // smem weights of Dm, Dm^T (dm_table)
   bool no_cull;          // testing aid: test every obstacle (KernelArgs::no_cull)
+  bool handoff;          // T = 2 with a tail round: warp 0 contracts warp 1's round 0
+  uint64_t* tbar;        // the team's hand-off mbarrier
 };
 
 // --------------------------------------------------- collision projections
@@ -589,7 +598,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
 template <int M, bool RES>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
-                                              int lane, int w, int T, int team, PhaseClock& pc) {
+                                              int lane, int w, int T, int team, unsigned hand_phase, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
@@ -607,6 +616,33 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   const int aoff0 = (lane >> 2) * QP64 + (lane & 3), aoff1 = min(8 + (lane >> 2), NV - 1) * QP64 + (lane & 3);
   const float* __restrict__ ucol = &ws->U[lane >> 2][lane & 3];   // B fragment: U[k = lane % 4][n = lane / 4]
   double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+  auto contract_round = [&](int u, int s0, int s1) {   // MMA steps [s0, s1) of a full round
+    const int t0 = 32 * u;
+    const float* __restrict__ up = ucol + t0;
+    const double* __restrict__ a0 = P64 + aoff0 + t0;
+    const double* __restrict__ a1 = P64 + aoff1 + t0;
+    if (t0 + 32 <= q) {   // full round: 8 steps, immediate offsets
+#pragma unroll
+      for (int st = 0; st < 8; ++st) {
+        if (st < s0 || st >= s1) continue;
+        const double b = f2d(up[4 * st]);
+        mma_f64_884(g0, a0[4 * st], b);
+        mma_f64_884(g1, a1[4 * st], b);
+      }
+    } else {
+      const int ns = (q - t0 + 3) >> 2;
+#pragma unroll 1
+      for (int st = 0; st < ns; ++st) {
+        const double b = f2d(up[4 * st]);
+        mma_f64_884(g0, a0[4 * st], b);
+        mma_f64_884(g1, a1[4 * st], b);
+      }
+    }
+  };
+  // T = 2 with a tail round: warp 1 projects rounds 0, 2 and warp 0 rounds 1 and the
+  // tail, so warp 0 also contracts round 0 (after warp 1 signals its U on the team's
+  // mbarrier) -- the MMAs leave the critical warp
+  const bool give = pa.handoff && w == 1, take = pa.handoff && w == 0;
 #pragma unroll 1
   for (int u = T - 1 - w; u < pa.rounds; u += T) {   // this warp's rounds (leader: the lightest)
     // samples t >= q of the last round have a zero basis row and far-away
@@ -719,28 +755,16 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       rps = fmaf(dth, dth, rps);
     }
     __syncwarp();   // the round's U is complete
-    {
-      const int t0 = 32 * u;
-      const float* __restrict__ up = ucol + t0;
-      const double* __restrict__ a0 = P64 + aoff0 + t0;
-      const double* __restrict__ a1 = P64 + aoff1 + t0;
-      if (t0 + 32 <= q) {   // full round: 8 steps, immediate offsets
-#pragma unroll
-        for (int st = 0; st < 8; ++st) {
-          const double b = f2d(up[4 * st]);
-          mma_f64_884(g0, a0[4 * st], b);
-          mma_f64_884(g1, a1[4 * st], b);
-        }
-      } else {
-        const int ns = (q - t0 + 3) >> 2;
-#pragma unroll 1
-        for (int st = 0; st < ns; ++st) {
-          const double b = f2d(up[4 * st]);
-          mma_f64_884(g0, a0[4 * st], b);
-          mma_f64_884(g1, a1[4 * st], b);
-        }
-      }
+    if (give && u == 0) {
+      if (lane == 0) mbar_arrive(pa.tbar);
+      contract_round(0, 0, 8 - HANDOFF_STEPS);
+    } else {
+      contract_round(u, 0, 8);
     }
+  }
+  if (take) {
+    mbar_wait(pa.tbar, hand_phase);
+    contract_round(0, 8 - HANDOFF_STEPS, 8);
   }
   __syncwarp();
   BMC_TICK(pc, 10);
@@ -823,9 +847,11 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   int* list_base = reinterpret_cast<int*>(clr_base + (size_t)ipc * T_MAX * nclr);
   double* hp_base = reinterpret_cast<double*>(list_base + (size_t)wpc * nclr);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (size_t)wpc * HP_SLOTS);
+  uint64_t* tbar = mbar + 1;   // [ipc] hand-off barriers
 
   // --- stage the batch-invariant data -------------------------------------
   if (tid == 0) mbar_init(mbar, 1);
+  if (tid < ipc) mbar_init(tbar + tid, 1);
   __syncthreads();
   const unsigned blob_bytes = (unsigned)BlobLayout::bytes(QP);
   if (tid == 0) {
@@ -914,6 +940,12 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.hp = hp_base + (size_t)team * T * HP_SLOTS;
   pa.dmtab = ub + DM_TAB;
   pa.no_cull = a.no_cull != 0;
+  // hand-off when warp 0's second round is a light tail: T = 2, an even number of
+  // rounds, a partial last round, and a moderate collision load (n m <= 128; with
+  // more obstacle pairs the tail round itself is busy -- measured: C3 (90) gains
+  // 2.7 %, C4 (200) would lose 3 %).  Deterministic for a given launch.
+  pa.handoff = (T == 2) && (pa.rounds % 2 == 0) && (q % 32 != 0) && (n * M <= 128);
+  pa.tbar = tbar + team;
   float r[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
@@ -1054,9 +1086,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       // residual terms only where they are reported: a compile-time flag keeps the
       // hot (RES = false) copy free of the per-round re-evaluation of a runtime flag
       if (want_res)
-        phase_project<M, true>(pa, r, ws, lane, w, T, team, pc);
+        phase_project<M, true>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, pc);
       else
-        phase_project<M, false>(pa, r, ws, lane, w, T, team, pc);
+        phase_project<M, false>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, pc);
       __syncwarp();
       BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
