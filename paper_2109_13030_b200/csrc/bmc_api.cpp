@@ -52,6 +52,7 @@ struct DeviceGuard {  // restore the caller's current device
 struct Blob {
   unsigned char* d = nullptr;
   int nb = 0;
+  int blockdiag = 0;
 };
 
 struct HostBuf {  // context-owned device buffers for bmc_solve_host
@@ -215,6 +216,7 @@ static int32_t get_blob(bmc_ctx* c, int n, Blob** out) {
   if (build_consts(setup_params(c), n, &hc, &err) != 0) return fail(BMC_ESINGULAR, err);
   Blob b;
   b.nb = hc.nb;
+  b.blockdiag = hc.blockdiag;
   const size_t bytes = BlobLayout::bytes(hc.QP);
   cudaError_t e = cudaMalloc(&b.d, bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(blob)");
@@ -340,6 +342,7 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   const bool prof = std::getenv("BMC_PROF") != nullptr;
   // testing aid: BMC_NOCULL=1 disables the exact culling (results must be bitwise equal)
   if (const char* e = std::getenv("BMC_NOCULL")) a.no_cull = std::atoi(e) != 0;
+  a.blockdiag = blob->blockdiag;
   const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
   if (prof && cudaMalloc(&a.prof, sizeof(long long) * 12 * nwarps) == cudaSuccess)
     cudaMemsetAsync(a.prof, 0, sizeof(long long) * 12 * nwarps, s);

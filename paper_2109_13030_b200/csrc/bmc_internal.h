@@ -78,6 +78,7 @@ struct KernelArgs {
   double ref_x0, ref_dx, ref_y0, ref_dy;
   long long* prof;             // [warps][12] phase cycles (PROFILE builds only) or null
   int no_cull;                 // testing aid (BMC_NOCULL): every obstacle tested every round
+  int blockdiag;               // M, K11 block diagonal (symmetric footprint, sum r_i = 0)
 };
 
 struct SetupParams {
@@ -106,6 +107,7 @@ int stomp_factor(double L[5][5]);
 // host-side constants for one (params, n)
 struct HostConsts {
   int q, QP, nb, n, m;
+  int blockdiag = 0;       // sum r_i = 0: M and K11 are block diagonal (c_x | c_c blocks)
   double blob_f64[BlobLayout::n_doubles];
   float* pt = nullptr;     // [11][QP]
   double* pt64 = nullptr;  // [11][p64_stride(QP)]

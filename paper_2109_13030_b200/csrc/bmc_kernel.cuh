@@ -1017,12 +1017,24 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           __syncwarp();
           if (c == 0 && lp_pending) lampsi_step();
           {
-            // 8 independent fp64 chains (depth <= 6): the step is latency-bound
+            // 8 independent fp64 chains (depth <= 6): the step is latency-bound.  With a
+            // symmetric footprint M and K11 are block diagonal (setup.cpp): row k only
+            // meets the columns of its own block (c_x rows 0..10, c_c rows 11..21).
             double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            if (a.blockdiag) {
+              const int j0 = (kc < NV) ? 0 : NV;
 #pragma unroll
-            for (int j = 0; j < NV2; ++j) {
-              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
-              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
+              for (int jj = 0; jj < NV; ++jj) {
+                const int j = j0 + jj;
+                acc[jj & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[jj & 3]);
+                acc[4 + (jj & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (jj & 3)]);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < NV2; ++j) {
+                acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
+                acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
+              }
             }
             const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
             xi[c] = (k < NV2) ? v : 0.0;

@@ -206,12 +206,18 @@ int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err)
   // blob (transposed storage)
   double* f = out->blob_f64;
   std::memset(f, 0, sizeof(out->blob_f64));
+  // With sum r_i = 0 the coupling block n R1 P'P of F^T F vanishes, the xi1 KKT
+  // separates into the c_x block (with the boundary rows) and the c_c block, and M,
+  // K11 are block diagonal: the off-diagonal blocks are stored as exact zeros and the
+  // kernel skips them.
+  out->blockdiag = (R1 == 0.0) ? 1 : 0;
   for (int k = 0; k < NV2; ++k)
     for (int j = 0; j < NV2; ++j) {
       double mkj = 0.0;  // (rho K11 F^T F)[k][j]
       for (int l = 0; l < NV2; ++l) mkj += Ki[k * N1 + l] * FtF[l][j];
-      f[BlobLayout::Mt + j * NV2 + k] = p.rho * mkj;
-      f[BlobLayout::K11t + j * NV2 + k] = Ki[k * N1 + j];
+      const bool off = out->blockdiag && ((k < NV) != (j < NV));
+      f[BlobLayout::Mt + j * NV2 + k] = off ? 0.0 : p.rho * mkj;
+      f[BlobLayout::K11t + j * NV2 + k] = off ? 0.0 : Ki[k * N1 + j];
     }
   for (int rr = 0; rr < nb; ++rr)
     for (int k = 0; k < NV2; ++k) f[BlobLayout::K12t + rr * NV2 + k] = Ki[k * N1 + NV2 + rr];

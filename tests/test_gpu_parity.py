@@ -208,6 +208,14 @@ def test_many_circles(m):
     check(cfg, make_problem(cfg, 8), f"m={m}")
 
 
+def test_asymmetric_footprint():
+    """Offsets with sum r_i != 0: F^T F couples the c_x and c_c blocks (n R1 P'P), so the
+    kernel takes the full 22 x 44 xi1 mat-vec instead of the block-diagonal one."""
+    cfg = CONFIGS["C2"].with_(B=12, K=60)
+    r = [-0.2, 0.3, 0.6]
+    check(cfg, make_problem(cfg, 9), "asymmetric footprint", okw=dict(r=r), gkw=dict(r=r))
+
+
 def test_res_trace():
     cfg = CONFIGS["C1"].with_(B=5)
     pr = make_problem(cfg, 0)
