@@ -54,31 +54,40 @@ constexpr int HP_SLOTS = 8 * 12; // per-warp partial contractions (D2), doubles
 #endif
 constexpr int HANDOFF_STEPS = BMC_HANDOFF_STEPS;   // MMA steps of round 0 that warp 0 takes (T = 2)
 
-// Per-instance state shared by the T warps of its team.  The x and y channels
-// of xi1 are decoupled in the xi1 step and the lambda step (Eq. 10: F and the
-// KKT are block diagonal over channels), so a team gives each channel to one
-// warp; the small heading step runs redundantly in every warp.
-struct WarpSmem {
+// Per-instance state shared by the TT warps of its team (per-warp arrays sized
+// by the compile-time team size: shared memory bounds the instances per SM for
+// large batches).  The x and y channels of xi1 are decoupled in the xi1 step and
+// the lambda step (Eq. 10: F and the KKT are block diagonal over channels), so a
+// team gives each channel to one warp; the small heading step runs redundantly
+// in every warp.
+template <int TT>
+struct alignas(16) WarpSmemT {
   double xi1[2][24];      // [ch][k] current xi1 (fp64), written by the channel's owner
   double rhs[2][24];      // [ch][k] lambda - rho h
   double h[2][24];        // [ch][k] F^T (F xi1 - g) (fp64: it cancels), owner-written
-  double xi2w[T_MAX][12]; // per-warp copies of xi2 (the heading step is redundant)
-  double rhspw[T_MAX][12];
+  double xi2w[TT][12];    // per-warp copies of xi2 (the heading step is redundant)
+  double rhspw[TT][12];
   // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
   // c_y - c_ref_y, Dm c_x, Dm c_y, Dm^2 c_x, Dm^2 c_y, c_c, c_s (Dm: the
   // derivative operator on coefficients, Pdot = P Dm)
   float cfi[NV + 1][8];
-  float cf4[T_MAX][12];   // per-warp fp32 c_psi
+  float cf4[TT][12];      // per-warp fp32 c_psi
   float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
-  double part_th[T_MAX][16];    // per-warp P^T theta partials, summed in warp order
-  float part_res[T_MAX][4];
-  float U[8][QP + 4];           // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2);
-                                // stride QP + 4: MMA B-fragment columns on distinct banks
+  double part_th[TT][16];       // per-warp P^T theta partials, summed in warp order
+  float part_res[TT][4];
+  alignas(16) float U[8][QP + 4];   // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2);
+                                // stride QP + 4: MMA B-fragment columns on distinct banks.
+                                // TT = 1: also the D2 partial slots once the round loop is done
   float prv[3][QP];             // x, y, psi at the previous evaluation (culling clock)
   float clk[T_MAX];             // per-round movement clocks (culling)
   float pad_[T_MAX];
 };
-static_assert(sizeof(WarpSmem) % 16 == 0, "WarpSmem must keep 16-byte alignment");
+static_assert(sizeof(WarpSmemT<1>) % 16 == 0 && sizeof(WarpSmemT<2>) % 16 == 0 && sizeof(WarpSmemT<4>) % 16 == 0,
+              "WarpSmem must keep 16-byte alignment");
+static_assert(HP_SLOTS * sizeof(double) <= sizeof(float) * 8 * (QP + 4), "D2 partials fit in U (TT = 1)");
+__host__ __device__ inline size_t ws_bytes(int T) {
+  return T == 1 ? sizeof(WarpSmemT<1>) : T == 2 ? sizeof(WarpSmemT<2>) : sizeof(WarpSmemT<4>);
+}
 
 // Team barrier: named barrier per team (id 1 + team) over its 32 T threads.
 __device__ __forceinline__ void team_sync(int team, int T) {
@@ -124,8 +133,9 @@ __host__ __device__ inline int clr_stride(int n) { return pad_obstacles(n) + JB;
 __host__ __device__ inline size_t smem_bytes(int n, int ipc, int T) {
   const int np = pad_obstacles(n) + 1;
   return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
-         U_DOUBLES * sizeof(double) + (size_t)ipc * sizeof(WarpSmem) +
-         (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) + (size_t)ipc * T * HP_SLOTS * sizeof(double) +
+         U_DOUBLES * sizeof(double) + (size_t)ipc * ws_bytes(T) +
+         (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) +
+         (T > 1 ? (size_t)ipc * T * HP_SLOTS * sizeof(double) : 0) +
          16 + (size_t)ipc * 8;
 }
 
@@ -502,6 +512,7 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
 constexpr float CULL_MARGIN = 2e-3f;
 
 // advance the round's clock by this evaluation's movement; returns the clock
+template <class WarpSmem>
 __device__ __forceinline__ float cull_tick(WarpSmem* ws, int u, int t, float x, float y, float psi, float rabs,
                                            int lane) {
   const float dx = x - ws->prv[0][t], dy = y - ws->prv[1][t], dp = psi - ws->prv[2][t];
@@ -548,6 +559,7 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
+template <class WarpSmem>
 __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
                                             WarpSmem* ws, int lane, int q, int w, int T) {
   float cc[NV], cs[NV];
@@ -596,7 +608,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 //   U0 = n R1 e_c - D_x, U1 = (n R2 + 1) e_c - E_x, U2, U3 likewise for y,
 //   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
-template <int M, bool RES>
+template <int M, bool RES, class WarpSmem>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
                                               int lane, int w, int T, int team, unsigned hand_phase, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
@@ -839,6 +851,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   const int npad = pad_obstacles(n), nclr = clr_stride(n);
   float4* abi = reinterpret_cast<float4*>(obs + (size_t)(npad + 1) * QP);
   double* ub = reinterpret_cast<double*>(abi + npad + 1);
+  using WarpSmem = WarpSmemT<TT>;
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
   constexpr int T = TT;                              // warps per instance (compile time: folds the
   const int ipc = wpc / T;                           // team bookkeeping), instances per CTA
@@ -846,7 +859,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   float* clr_base = reinterpret_cast<float*>(wsbase + ipc);
   int* list_base = reinterpret_cast<int*>(clr_base + (size_t)ipc * T_MAX * nclr);
   double* hp_base = reinterpret_cast<double*>(list_base + (size_t)wpc * nclr);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (size_t)wpc * HP_SLOTS);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (TT > 1 ? (size_t)wpc * HP_SLOTS : 0));
   uint64_t* tbar = mbar + 1;   // [ipc] hand-off barriers
 
   // --- stage the batch-invariant data -------------------------------------
@@ -888,8 +901,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   }
   for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
     (&wsbase[i / ((NV + 1) * 8)].cfi[0][0])[i % ((NV + 1) * 8)] = 0.f;
-  for (int i = tid; i < ipc * T_MAX * 12; i += blockDim.x)
-    (&wsbase[i / (T_MAX * 12)].cf4[0][0])[i % (T_MAX * 12)] = 0.f;
+  for (int i = tid; i < ipc * TT * 12; i += blockDim.x)
+    (&wsbase[i / (TT * 12)].cf4[0][0])[i % (TT * 12)] = 0.f;
   for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
   for (int i = tid; i < ipc * (3 * QP + 2 * T_MAX); i += blockDim.x)
     (&wsbase[i / (3 * QP + 2 * T_MAX)].prv[0][0])[i % (3 * QP + 2 * T_MAX)] = 0.f;
@@ -937,7 +950,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.nclr = nclr;
   pa.clr = clr_base + (size_t)team * T_MAX * nclr;
   pa.list = list_base + (size_t)warp * nclr;
-  pa.hp = hp_base + (size_t)team * T * HP_SLOTS;
+  pa.hp = (TT > 1) ? hp_base + (size_t)team * T * HP_SLOTS : reinterpret_cast<double*>(&wsbase[team].U[0][0]);
   pa.dmtab = ub + DM_TAB;
   pa.no_cull = a.no_cull != 0;
   // hand-off when warp 0's second round is a light tail: T = 2, an even number of
