@@ -344,26 +344,38 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   if (const char* e = std::getenv("BMC_NOCULL")) a.no_cull = std::atoi(e) != 0;
   a.blockdiag = blob->blockdiag;
   const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
-  if (prof && cudaMalloc(&a.prof, sizeof(long long) * 12 * nwarps) == cudaSuccess)
-    cudaMemsetAsync(a.prof, 0, sizeof(long long) * 12 * nwarps, s);
+  if (prof && cudaMalloc(&a.prof, sizeof(long long) * 16 * nwarps) == cudaSuccess)
+    cudaMemsetAsync(a.prof, 0, sizeof(long long) * 16 * nwarps, s);
   cudaError_t e = launch_am(a, wpc, s);
   c->last_launches = 1;
   if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");
   if (prof && a.prof) {
-    std::vector<long long> hp(12 * nwarps);
+    std::vector<long long> hp(16 * nwarps);
     cudaStreamSynchronize(s);
     cudaMemcpy(hp.data(), a.prof, sizeof(long long) * hp.size(), cudaMemcpyDeviceToHost);
     cudaFree(a.prof);
-    const char* names[12] = {"A", "bar1", "B", "bar2", "C", "D2mma", "bar3", "D2+", "E", "tested", "D1", "needed"};
+    const char* names[16] = {"A", "bar1", "B", "bar2", "C", "D2mma", "bar3", "D2+", "E", "tested", "D1", "needed",
+                             "D1eval", "D1cull", "D1coll", "D1U+mma"};
     for (int role = 0; role < team; ++role) {
-      double tot[12] = {0};
+      double tot[16] = {0};
       long long cnt = 0;
       for (long long wv = role; wv < nwarps; wv += team, ++cnt)
-        for (int i = 0; i < 12; ++i) tot[i] += (double)hp[wv * 12 + i];
+        for (int i = 0; i < 16; ++i) tot[i] += (double)hp[wv * 16 + i];
       std::fprintf(stderr, "[bmc prof] team=%d ipc=%d warp-role %d cycles/iter:", team, ipc, role);
-      for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %s=%.1f", names[i], tot[i] / cnt / (pr->iters + 1));
+      for (int i = 0; i < 16; ++i) std::fprintf(stderr, " %s=%.1f", names[i], tot[i] / cnt / (pr->iters + 1));
       std::fprintf(stderr, "\n");
     }
+    // per team slot of the CTA (warp ids rise with the slot): loop cycles per iteration
+    std::fprintf(stderr, "[bmc prof] loop cycles/iter by team slot:");
+    for (int slot = 0; slot < ipc; ++slot) {
+      double tot = 0.0;
+      long long cnt = 0;
+      for (long long wv = (long long)slot * team; wv < nwarps; wv += (long long)ipc * team, ++cnt)
+        for (int i = 0; i <= 10; ++i)
+          if (i != 9) tot += (double)hp[wv * 16 + i];
+      std::fprintf(stderr, " %.0f", tot / cnt / (pr->iters + 1));
+    }
+    std::fprintf(stderr, "\n");
   }
   return BMC_OK;
 }

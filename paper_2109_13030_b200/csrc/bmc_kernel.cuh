@@ -64,7 +64,6 @@ template <int TT>
 struct alignas(16) WarpSmemT {
   double xi1[2][24];      // [ch][k] current xi1 (fp64), written by the channel's owner
   double rhs[2][24];      // [ch][k] lambda - rho h
-  double h[2][24];        // [ch][k] F^T (F xi1 - g) (fp64: it cancels), owner-written
   double xi2w[TT][12];    // per-warp copies of xi2 (the heading step is redundant)
   double rhspw[TT][12];
   // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
@@ -72,13 +71,15 @@ struct alignas(16) WarpSmemT {
   // derivative operator on coefficients, Pdot = P Dm)
   float cfi[NV + 1][8];
   float cf4[TT][12];      // per-warp fp32 c_psi
-  float c[QP], s[QP], th[QP];   // copies c, s and theta per sample
+  float2 cs[QP];                // copies (c, s) per sample
+  float th[QP];                 // theta per sample
   double part_th[TT][16];       // per-warp P^T theta partials, summed in warp order
   float part_res[TT][4];
   alignas(16) float U[8][QP + 4];   // per-sample vectors of F^T (F xi1 - g) (phase D1 -> D2);
                                 // stride QP + 4: MMA B-fragment columns on distinct banks.
                                 // TT = 1: also the D2 partial slots once the round loop is done
-  float prv[3][QP];             // x, y, psi at the previous evaluation (culling clock)
+  float2 pxy[QP];               // x, y and psi at the previous evaluation (culling clock)
+  float ppsi[QP];
   float clk[T_MAX];             // per-round movement clocks (culling)
   float pad_[T_MAX];
 };
@@ -105,9 +106,11 @@ constexpr int DM_TAB = 56;
 
 // Development aid (make PROFILE=1): per-warp cycle counts of each phase.
 #ifdef BMC_PROFILE
+constexpr int PROF_SLOTS = 16;
 struct PhaseClock {
-  long long acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long acc[PROF_SLOTS] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = 0;
+  long long s0 = 0;   // sub-phase timer (does not move t0)
 };
 #define BMC_TICK(pc, i)                  \
   do {                                   \
@@ -115,9 +118,17 @@ struct PhaseClock {
     (pc).acc[i] += t1_ - (pc).t0;        \
     (pc).t0 = t1_;                       \
   } while (0)
+// sub-phase split of D1 (slots 12..15) on its own timer
+#define BMC_SUB(pc, i)                   \
+  do {                                   \
+    const long long t1_ = clock64();     \
+    if ((i) >= 0) (pc).acc[i] += t1_ - (pc).s0; \
+    (pc).s0 = t1_;                       \
+  } while (0)
 #else
 struct PhaseClock {};
 #define BMC_TICK(pc, i) ((void)0)
+#define BMC_SUB(pc, i) ((void)0)
 #endif
 
 // obstacles are padded to a multiple of JB with far-away, zero-radius dummies
@@ -189,6 +200,21 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// Packed fp32 pairs (FFMA2 / FADD2 / FMUL2, sm_100): one instruction for two
+// lanes' worth of fp32 work, each half rounded exactly like the scalar op, so
+// pairing changes no result bit.
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {   // one FADD2 with a negated operand
+  float2 d;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&d))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 
 // FP64 tensor-core MMA D = A B + D, m8n8k4 (A row-major 8x4, B col-major 4x8):
 // a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
@@ -357,12 +383,11 @@ struct Proj {
   const float* Pt;       // smem basis [3][11][QP]
   const double* Pt64;    // the same basis in fp64 (contractions)
   const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
-  const float4* abi;     // smem (a, b, a^2 or ab, kind) per obstacle
+  const float4* abi;     // smem (a, b, a b, kind) per obstacle
   int q, n, rounds;
   bool all_circ;
   float nR1, nR2p1, v_max, a_max;
-  float rlo, rhi;        // extent of the circle offsets along the heading
-  float rabs;            // max(|rlo|, |rhi|)
+  float rabs;            // max_i |r_i| (culling clock)
   float* clr;            // smem clearance stamps of the instance, [4 rounds][nclr]
   int* list;             // smem active list of the warp, [nclr]
   int npad, nclr;        // padded obstacle count (index npad = far dummy), stride
@@ -385,79 +410,57 @@ struct Proj {
 // The residual terms (r_i e - delta)^2 are accumulated as
 // base + delta (delta - 2 r_i e), with base = sum_i (r_i e)^2 per obstacle.
 //
-// Circular obstacles: delta = 0 unless |(x~, y~)| < a, so blocks of JB
-// obstacles are first tested (x~, y~, |.|^2 only); a warp-wide OR of the
-// per-lane inside masks selects the obstacles whose closed form (rsqrt on
-// the MUFU pipe) must run.
-//
-// The first pass tests the segment of circle centres {x + r u : r in
-// [rlo, rhi]}, u = (cos psi, sin psi), instead of each centre: with
-// d = x - o, min_r |d + r u|^2 = D0 + 2 r* B + r*^2, D0 = |d|^2, B = d.u,
-// r* = clamp(-B, rlo, rhi) -- a lower bound of every centre's distance, so the
-// test is conservative (exact cases only ever go to the second pass) and
-// costs the same for any number of circles.
-//
-// Only the obstacles of the round's active list are visited (see
-// `build_active`); the pass records, per visited obstacle, the round's
-// clearance min_t |segment - o_j| - a_j stamped with the movement clock A.
+// Circular obstacles (coll_circ): delta = 0 unless |(x~, y~)| < a, and the
+// closed form max(a / |(x~, y~)| - 1, 0) is exactly zero outside, so every
+// obstacle of the round's active list (see `build_active`) runs it at all M
+// circle centres: no inside test, no warp vote, no data-dependent branch (an
+// earlier variant tested the segment of circle centres first and ran the
+// closed form only where some lane was inside; this one has fewer dependent
+// steps per obstacle and the same result bits).  The pass records, per
+// visited obstacle, the round's clearance min over samples and circles of
+// |centre - o_j| - a_j, stamped with the movement clock A.
 template <int M>
-__device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __restrict__ ob, const float4* __restrict__ abi,
-                                          const int* __restrict__ list, int na, float* __restrict__ clr, float A,
-                                          int lane, const float (&X)[M], const float (&Y)[M],
-                                          float xc, float yc, float cu, float su, float rlo, float rhi,
-                                          const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
-                                          float (&Dy)[M], float& rc, long long* prof_need = nullptr) {
-  unsigned any_need = 0u;   // warp-uniform: some closed form ran
+__device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __restrict__ ob,
+                                              const float4* __restrict__ abi, const int* __restrict__ list, int na,
+                                              float* __restrict__ clr, float A, int lane, const float2 (&XY)[M],
+                                              const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
+                                              float& rc) {
 #pragma unroll 1
   for (int jb = 0; jb < na; jb += JB) {
-    unsigned mask = 0u, qm = 0u;
+    float r2m[JB];
+    // the JB closed forms first (one basic block: their loads and MUFU latencies
+    // overlap), the warp reductions of the stamps after them
 #pragma unroll
     for (int jj = 0; jj < JB; ++jj) {
       const int j = list[jb + jj];   // the list is padded to a multiple of JB with a far dummy
       const float2 o = ob[j * QP];
-      const float thr = abi[j].z;   // a^2 (1 + 1e-5) + 1e-5
-      const float dx = xc - o.x, dy = yc - o.y;
-      const float d0 = fmaf(dy, dy, dx * dx), bd = fmaf(dy, su, dx * cu);
-      const float rs = fmaxf(rlo, fminf(rhi, -bd));
-      const float qmin = fmaf(rs, fmaf(2.f, bd, rs), d0);
-      // margin: absolute rounding of qmin is < 1e-6 m^2 for any obstacle within reach
-      mask |= (qmin < thr) ? (1u << jj) : 0u;
-      // round minimum of qmin (non-negative floats order as their bit patterns)
-      const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(fmaxf(qmin, 0.f)));
+      const float a = abi[j].x;
+      float r2min = INFINITY;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const float2 tt = sub2(XY[i], o);   // (x~, y~)
+        const float r2 = fmaf(tt.y, tt.y, tt.x * tt.x);
+        const float sc = fmaxf(fmaf(a, rsqrt_ftz(r2), -1.f), 0.f);
+        const float2 dd = mul2(bc2(sc), tt);
+        D[i] = add2(D[i], dd);
+        if (RES) rc = fmaf(dd.x, dd.x - 2.f * rec[i], fmaf(dd.y, dd.y - 2.f * res_s[i], rc));
+        r2min = fminf(r2min, r2);
+      }
+      r2m[jj] = r2min;
+    }
+    unsigned qm = 0u;
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      // round minimum (non-negative floats order as their bit patterns)
+      const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(r2m[jj]));
       qm = (lane == jj) ? mn : qm;
     }
     if (lane < JB) {
       const int j = list[jb + lane];
       clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
     }
-    const unsigned need = __reduce_or_sync(FULL, mask);
-    any_need |= need;
-#ifdef BMC_PROFILE
-    if (prof_need) *prof_need += __popc(need);
-#endif
-    {
-      unsigned nd = need;
-      while (nd) {
-        const int jj = __ffs(nd) - 1;
-        nd &= nd - 1;
-        const int j = list[jb + jj];
-        if ((mask >> jj) & 1u) {
-          const float2 o = ob[j * QP];
-          const float a = abi[j].x;
-#pragma unroll
-          for (int i = 0; i < M; ++i) {
-            const float xt = X[i] - o.x, yt = Y[i] - o.y;
-            const float sc = fmaxf(fmaf(a, rsqrt_ftz(fmaf(yt, yt, xt * xt)), -1.f), 0.f);
-            const float dx = sc * xt, dy = sc * yt;
-            Dx[i] += dx;
-            Dy[i] += dy;
-            if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
-          }
-        }
-      }
-    }
   }
-  return any_need;
+  return na > 0 ? 1u : 0u;
 }
 
 // Any obstacle kinds, one obstacle at a time.  GUARD handles x~ = y~ = 0
@@ -465,9 +468,9 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
 template <int M>
 __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, const float2* __restrict__ ob,
                                              const float4* __restrict__ abi,
-                                             int n, int g, int S, const float (&X)[M], const float (&Y)[M],
-                                             const float (&rec)[M], const float (&res_s)[M], float (&Dx)[M],
-                                             float (&Dy)[M], float& rc) {
+                                             int n, int g, int S, const float2 (&XY)[M],
+                                             const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
+                                             float& rc) {
 #pragma unroll 1
   for (int j = g; j < n; j += S) {
     const float2 o = ob[j * QP];
@@ -475,7 +478,7 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
     const float a = ab.x, b = ab.y;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      const float xt = X[i] - o.x, yt = Y[i] - o.y;
+      const float xt = XY[i].x - o.x, yt = XY[i].y - o.y;
       const float x2 = xt * xt, y2 = yt * yt;
       float dx, dy;
       if (ab.w == 1.f) {
@@ -491,8 +494,8 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
         dy = sc * yt;
       }
       if (GUARD && x2 + y2 == 0.f) { dx = a; dy = 0.f; }
-      Dx[i] += dx;
-      Dy[i] += dy;
+      D[i].x += dx;
+      D[i].y += dy;
       if (RES) rc = fmaf(dx, dx - 2.f * rec[i], fmaf(dy, dy - 2.f * res_s[i], rc));
     }
   }
@@ -500,7 +503,7 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
 
 // ------------------------------------------------------ temporal culling
 // Every iteration moves the circle centres of sample t by at most
-//   |(dx, dy)| + max(|rlo|, |rhi|) |dpsi|        (|d cos psi| <= |d psi|)
+//   |(dx, dy)| + max_i |r_i| |dpsi|        (|d cos psi| <= |d psi|)
 // where (dx, dy, dpsi) is the change of the evaluated x, y, psi since the
 // previous evaluation.  A per-(instance, round) clock A sums the warp maximum of
 // this bound over the iterations.  An obstacle whose stamped clearance
@@ -511,44 +514,26 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
 // deviations up to 1 km).
 constexpr float CULL_MARGIN = 2e-3f;
 
-// advance the round's clock by this evaluation's movement; returns the clock
-template <class WarpSmem>
-__device__ __forceinline__ float cull_tick(WarpSmem* ws, int u, int t, float x, float y, float psi, float rabs,
-                                           int lane) {
-  const float dx = x - ws->prv[0][t], dy = y - ws->prv[1][t], dp = psi - ws->prv[2][t];
-  ws->prv[0][t] = x;
-  ws->prv[1][t] = y;
-  ws->prv[2][t] = psi;
-  // |.| of a NaN keeps a NaN bit pattern, which is above +inf: the clock becomes NaN
-  const float mv = fmaf(rabs, fabsf(dp), sqrt_approx(fmaf(dx, dx, dy * dy)) * 1.000001f);
-  const float mx = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(fabsf(mv))));
-  const float A = ws->clk[u] + mx;
-  __syncwarp();
-  if (lane == 0) ws->clk[u] = A;
-  return A;
-}
-
 // Active list of one round: obstacles whose clearance no longer covers the
 // movement since it was stamped, padded to a multiple of JB with the far dummy
 // `npad`.  Returns the padded length.
 __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* __restrict__ list, int npad,
-                                            float A, int lane) {
+                                            float lim, int lane) {
   int na = 0;
-  const float lim = A + CULL_MARGIN;
   if (npad <= 32) {   // the common case: one ballot
-    const bool act = (lane < npad) && !(clr[lane] > lim);
+    const bool act = (lane < npad) && !(clr[lane] > lim);   // NaN clock or stamp: active
     const unsigned bal = __ballot_sync(FULL, act);
     if (act) list[__popc(bal & ((1u << lane) - 1u))] = lane;
     na = __popc(bal);
   } else {
 #pragma unroll 1
-  for (int j0 = 0; j0 < npad; j0 += 32) {
-    const int j = j0 + lane;
-    const bool act = (j < npad) && !(clr[j] > lim);   // NaN clock or stamp: active
-    const unsigned bal = __ballot_sync(FULL, act);
-    if (act) list[na + __popc(bal & ((1u << lane) - 1u))] = j;
-    na += __popc(bal);
-  }
+    for (int j0 = 0; j0 < npad; j0 += 32) {
+      const int j = j0 + lane;
+      const bool act = (j < npad) && !(clr[j] > lim);
+      const unsigned bal = __ballot_sync(FULL, act);
+      if (act) list[na + __popc(bal & ((1u << lane) - 1u))] = j;
+      na += __popc(bal);
+    }
   }
   const int nap = (na + JB - 1) & ~(JB - 1);
   if (lane < nap - na) list[na + lane] = npad;
@@ -562,13 +547,9 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
 template <class WarpSmem>
 __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
                                             WarpSmem* ws, int lane, int q, int w, int T) {
-  float cc[NV], cs[NV];
+  float2 ccs[NV];   // (c_c, c_s) per Bernstein index
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const float2 v = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
-    cc[k] = v.x;
-    cs[k] = v.y;
-  }
+  for (int k = 0; k < NV; ++k) ccs[k] = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
   double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
@@ -581,15 +562,11 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     float p[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
-    float c = 0.f, s = 0.f;
+    float2 cs = make_float2(0.f, 0.f);   // (c, s) = (P c_c, P c_s)
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      c = fmaf(p[k], cc[k], c);
-      s = fmaf(p[k], cs[k], s);
-    }
-    const float tht = atan2_fast(s, c);   // atan2(0, 0) = 0 (G18)
-    ws->c[t] = c;
-    ws->s[t] = s;
+    for (int k = 0; k < NV; ++k) cs = fma2(bc2(p[k]), ccs[k], cs);
+    const float tht = atan2_fast(cs.y, cs.x);   // atan2(0, 0) = 0 (G18)
+    ws->cs[t] = cs;
     ws->th[t] = tht;
     const double thd = f2d(tht);
 #pragma unroll
@@ -610,7 +587,8 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
 template <int M, bool RES, class WarpSmem>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
-                                              int lane, int w, int T, int team, unsigned hand_phase, PhaseClock& pc) {
+                                              int lane, int w, int T, int team, unsigned hand_phase, double (&hreg)[2],
+                                              float& clkreg, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
   float res = 0.f, rps = 0.f;
@@ -627,7 +605,8 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   const double* __restrict__ P64 = pa.Pt64;
   const int aoff0 = (lane >> 2) * QP64 + (lane & 3), aoff1 = min(8 + (lane >> 2), NV - 1) * QP64 + (lane & 3);
   const float* __restrict__ ucol = &ws->U[lane >> 2][lane & 3];   // B fragment: U[k = lane % 4][n = lane / 4]
-  double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+  // two accumulator sets (even / odd MMA steps): dependent chains of 4, not 8
+  double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
   auto contract_round = [&](int u, int s0, int s1) {   // MMA steps [s0, s1) of a full round
     const int t0 = 32 * u;
     const float* __restrict__ up = ucol + t0;
@@ -638,8 +617,13 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       for (int st = 0; st < 8; ++st) {
         if (st < s0 || st >= s1) continue;
         const double b = f2d(up[4 * st]);
-        mma_f64_884(g0, a0[4 * st], b);
-        mma_f64_884(g1, a1[4 * st], b);
+        if (st & 1) {
+          mma_f64_884(e0, a0[4 * st], b);
+          mma_f64_884(e1, a1[4 * st], b);
+        } else {
+          mma_f64_884(g0, a0[4 * st], b);
+          mma_f64_884(g1, a1[4 * st], b);
+        }
       }
     } else {
       const int ns = (q - t0 + 3) >> 2;
@@ -661,8 +645,11 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     // obstacle slots: they project to nothing and are excluded from the sums
     const int t = 32 * u + lane;
     const bool valid = t < q;
+    BMC_SUB(pc, -1);
     // x = P c, xdot = Pdot c = P (Dm c), xddot = P (Dm^2 c): one basis row per k
-    float x = 0.f, y = 0.f, xd = 0.f, yd = 0.f, xdd = 0.f, ydd = 0.f, psi = 0.f;
+    // (x, y), (xdot, ydot), (xddot, yddot) as fp32 pairs (FFMA2), psi scalar
+    float2 xy = make_float2(0.f, 0.f), xyd = xy, xydd = xy;
+    float psi = 0.f;
     {
       float cp[NV];
       load12(ws->cf4[w], cp);
@@ -671,31 +658,32 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
         const float p = Pt[k * QP + t];
         const float4 c0 = *reinterpret_cast<const float4*>(&ws->cfi[k][0]);
         const float2 c1 = *reinterpret_cast<const float2*>(&ws->cfi[k][4]);
-        x = fmaf(p, c0.x, x);
-        y = fmaf(p, c0.y, y);
-        xd = fmaf(p, c0.z, xd);
-        yd = fmaf(p, c0.w, yd);
-        xdd = fmaf(p, c1.x, xdd);
-        ydd = fmaf(p, c1.y, ydd);
+        xy = fma2(bc2(p), make_float2(c0.x, c0.y), xy);
+        xyd = fma2(bc2(p), make_float2(c0.z, c0.w), xyd);
+        xydd = fma2(bc2(p), c1, xydd);
         psi = fmaf(p, cp[k], psi);
       }
     }
+    const float x = xy.x, y = xy.y;
     // velocity / acceleration: g = projection onto the bound disk (G6, G7)
-    const float sv = fminf(fmaf(pa.v_max, rsqrt_ftz(fmaf(yd, yd, xd * xd)), -1.f), 0.f);
-    const float sa = fminf(fmaf(pa.a_max, rsqrt_ftz(fmaf(ydd, ydd, xdd * xdd)), -1.f), 0.f);
-    const float dvx = xd * sv, dvy = yd * sv, dax = xdd * sa, day = ydd * sa;
+    // negated offsets -(g - v) = v max(1 - v_max / |v|, 0) (bitwise the negation of the
+    // offset v min(v_max / |v| - 1, 0))
+    const float nsv = fmaxf(fmaf(-pa.v_max, rsqrt_ftz(fmaf(xyd.y, xyd.y, xyd.x * xyd.x)), 1.f), -0.f);
+    const float nsa = fmaxf(fmaf(-pa.a_max, rsqrt_ftz(fmaf(xydd.y, xydd.y, xydd.x * xydd.x)), 1.f), -0.f);
+    const float2 dv = mul2(xyd, bc2(nsv)), da = mul2(xydd, bc2(nsa));
+    const float dvx = dv.x, dvy = dv.y, dax = da.x, day = da.y;   // negated offsets
     if (RES && valid) res += dvx * dvx + dvy * dvy + dax * dax + day * day;
-    float sp, cps;
-    sincos_fast(psi, &sp, &cps);
-    const float ec = ws->c[t] - cps, es = ws->s[t] - sp;
-    float X[M], Y[M], Dx[M], Dy[M], rec[M], res_s[M];
+    float2 hd;   // heading (cos psi, sin psi)
+    sincos_fast(psi, &hd.y, &hd.x);
+    const float2 ecs = sub2(ws->cs[t], hd);   // (c - cos psi, s - sin psi)
+    const float ec = ecs.x, es = ecs.y;
+    float2 XY[M], D[M];
+    float rec[M], res_s[M];
     float base = 0.f;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      X[i] = fmaf(r[i], cps, x);
-      Y[i] = fmaf(r[i], sp, y);
-      Dx[i] = 0.f;
-      Dy[i] = 0.f;
+      XY[i] = fma2(bc2(r[i]), hd, xy);   // circle centre (x + r_i cos psi, y + r_i sin psi)
+      D[i] = make_float2(0.f, 0.f);
       rec[i] = 0.f;
       res_s[i] = 0.f;
     }
@@ -709,6 +697,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     }
     float rc = 0.f;
     const float2* ob = pa.obs + t;
+    BMC_SUB(pc, 12);   // evaluation, velocity / acceleration, heading
     // circular obstacles: culled, blocked inside test (coll_circ); ellipses:
     // the plain loop.  A non-finite result (x~ = y~ = 0 exactly, G18, rare)
     // reruns the plain loop with the guard; one call site keeps the hot loop
@@ -717,49 +706,57 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     bool exact = general;   // warp-uniform: some closed form ran (only those can be non-finite)
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
-      const float A = cull_tick(ws, u, t, x, y, psi, pa.rabs, lane);
-      const int na = build_active(clr, pa.list, pa.npad, pa.no_cull ? INFINITY : A, lane);
+      const float clk0 = __shfl_sync(FULL, clkreg, u);
+      // movement bound of this evaluation (see "temporal culling") -> the round's clock
+      const float2 dxy = sub2(xy, ws->pxy[t]);
+      const float ppsi0 = ws->ppsi[t];
+      ws->pxy[t] = xy;
+      ws->ppsi[t] = psi;
+      const float2 sq = mul2(dxy, dxy);
+      // |.| of a NaN keeps a NaN bit pattern, which is above +inf: the clock becomes NaN
+      const float mv = fmaf(pa.rabs, fabsf(psi - ppsi0), sqrt_approx(sq.x + sq.y) * 1.000001f);
+      const float A = clk0 + __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(fabsf(mv))));
+      if (lane == u) clkreg = A;
+      const int na = build_active(clr, pa.list, pa.npad, pa.no_cull ? INFINITY : A + CULL_MARGIN, lane);
 #ifdef BMC_PROFILE
       pc.acc[9] += na;
 #endif
-      long long* pneed = nullptr;
-#ifdef BMC_PROFILE
-      pneed = &pc.acc[11];
-#endif
-      exact = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, X, Y, x, y, cps, sp, pa.rlo, pa.rhi, rec,
-                           res_s, Dx, Dy, rc, pneed) != 0u;
+      BMC_SUB(pc, 13);   // culling clock and active list
+      exact = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
     }
     bool guard = false;
 #pragma unroll 1
     for (;;) {
-      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, X, Y, rec, res_s, Dx, Dy, rc);
+      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
+      if (guard || !exact) break;
       float chk = rc;
 #pragma unroll
-      for (int i = 0; i < M; ++i) chk += Dx[i] + Dy[i];
-      if (guard || !exact || !__any_sync(FULL, !isfinite(chk))) break;
+      for (int i = 0; i < M; ++i) chk += D[i].x + D[i].y;
+      if (!__any_sync(FULL, !isfinite(chk))) break;
 #pragma unroll
-      for (int i = 0; i < M; ++i) { Dx[i] = 0.f; Dy[i] = 0.f; }
+      for (int i = 0; i < M; ++i) D[i] = make_float2(0.f, 0.f);
       rc = 0.f;
       guard = true;
       general = true;
     }
-    float Ds_x = 0.f, Ds_y = 0.f, Ex = 0.f, Ey = 0.f;
+    BMC_SUB(pc, 14);   // collision projections
+    float2 nDs = make_float2(0.f, 0.f), nE = nDs;   // -sum_i delta_i, -sum_i r_i delta_i
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      Ds_x += Dx[i];
-      Ds_y += Dy[i];
-      Ex = fmaf(r[i], Dx[i], Ex);
-      Ey = fmaf(r[i], Dy[i], Ey);
+      nDs = sub2(nDs, D[i]);
+      nE = fma2(bc2(-r[i]), D[i], nE);
     }
     {
-      ws->U[0][t] = fmaf(pa.nR1, ec, -Ds_x);
-      ws->U[1][t] = fmaf(pa.nR2p1, ec, -Ex);
-      ws->U[2][t] = fmaf(pa.nR1, es, -Ds_y);
-      ws->U[3][t] = fmaf(pa.nR2p1, es, -Ey);
-      ws->U[4][t] = -dvx;
-      ws->U[5][t] = -dax;
-      ws->U[6][t] = -dvy;
-      ws->U[7][t] = -day;
+      const float2 u02 = fma2(bc2(pa.nR1), ecs, nDs);
+      const float2 u13 = fma2(bc2(pa.nR2p1), ecs, nE);
+      ws->U[0][t] = u02.x;
+      ws->U[1][t] = u13.x;
+      ws->U[2][t] = u02.y;
+      ws->U[3][t] = u13.y;
+      ws->U[4][t] = dvx;   // -(g_v - v): the velocity / acceleration offsets are stored negated
+      ws->U[5][t] = dax;
+      ws->U[6][t] = dvy;
+      ws->U[7][t] = day;
     }
     if (valid) {
       if (RES) res += fmaf((float)n, base, rc) + ec * ec + es * es;
@@ -773,6 +770,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     } else {
       contract_round(u, 0, 8);
     }
+    BMC_SUB(pc, 15);   // U and the round's MMAs
   }
   if (take) {
     mbar_wait(pa.tbar, hand_phase);
@@ -784,11 +782,11 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   {
     const int g8 = lane >> 2, c4 = lane & 3;
     double* hp = pa.hp + w * HP_SLOTS;
-    hp[(2 * c4) * 12 + g8] = g0[0];
-    hp[(2 * c4 + 1) * 12 + g8] = g0[1];
+    hp[(2 * c4) * 12 + g8] = g0[0] + e0[0];
+    hp[(2 * c4 + 1) * 12 + g8] = g0[1] + e0[1];
     if (8 + g8 < NV) {
-      hp[(2 * c4) * 12 + 8 + g8] = g1[0];
-      hp[(2 * c4 + 1) * 12 + 8 + g8] = g1[1];
+      hp[(2 * c4) * 12 + 8 + g8] = g1[0] + e1[0];
+      hp[(2 * c4 + 1) * 12 + 8 + g8] = g1[1] + e1[1];
     }
   }
   if (RES) {   // residual partials must be visible to the team before the barrier
@@ -808,8 +806,9 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   //   h_copy = P^T U1                                          (x; y: U3)
   const int nch = (T == 1) ? 2 : (w < 2 ? 1 : 0);
   const int k = lane;
-#pragma unroll 1
-  for (int ci = 0; ci < nch; ++ci) {
+#pragma unroll
+  for (int ci = 0; ci < 2; ++ci) {   // unrolled: hreg stays in registers
+    if (ci >= nch) break;
     const int ch = (T == 1) ? ci : w;
     // lanes k < 11: (P^T U)[k] of U0/U2 (gp), U4/U6 (gv), U5/U7 (ga);
     // lanes 11..21: gp = (P^T U1/U3)[k - 11].  Branch-free: other lanes read
@@ -829,7 +828,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     // Dm^T gv + Dm^T Dm^T ga = Dm^T (gv + Dm^T ga)
     const double z = dmT_apply(ga, pa.dmtab, k) + gv;
     const double d = dmT_apply(z, pa.dmtab, k);
-    if (k < NV2) ws->h[ch][k] = (k < NV) ? gp + d : gp;
+    hreg[ci] = (k < NV) ? gp + d : gp;   // lane k holds h[k] (k < 22) of its channel
   }
 }
 
@@ -894,9 +893,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
-    // z: circles -> the inside-test threshold a^2 (1 + 1e-5) + 1e-5 m^2 (coll_circ; covers
-    // the fp32 rounding of the segment distance), ellipses -> a b (scaled rule)
-    abi[j] = make_float4(aa, bb, kind == 0.f ? fmaf(aa * aa, 1.00001f, 1e-5f) : aa * bb, kind);
+    // z: a b (numerator of the scaled rule, coll_general)
+    abi[j] = make_float4(aa, bb, aa * bb, kind);
     circ &= (aa == bb);
   }
   for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
@@ -905,7 +903,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     (&wsbase[i / (TT * 12)].cf4[0][0])[i % (TT * 12)] = 0.f;
   for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
   for (int i = tid; i < ipc * (3 * QP + 2 * T_MAX); i += blockDim.x)
-    (&wsbase[i / (3 * QP + 2 * T_MAX)].prv[0][0])[i % (3 * QP + 2 * T_MAX)] = 0.f;
+    (&wsbase[i / (3 * QP + 2 * T_MAX)].pxy[0].x)[i % (3 * QP + 2 * T_MAX)] = 0.f;
   const bool all_circ = __syncthreads_and(circ);
   mbar_wait(mbar, 0);
   __syncthreads();
@@ -939,13 +937,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.nR2p1 = a.nR2p1;
   pa.v_max = a.v_max;
   pa.a_max = a.a_max;
-  pa.rlo = a.r[0];
-  pa.rhi = a.r[0];
-  for (int i = 1; i < M; ++i) {
-    pa.rlo = fminf(pa.rlo, a.r[i]);
-    pa.rhi = fmaxf(pa.rhi, a.r[i]);
-  }
-  pa.rabs = fmaxf(fabsf(pa.rlo), fabsf(pa.rhi));
+  pa.rabs = 0.f;
+  for (int i = 0; i < M; ++i) pa.rabs = fmaxf(pa.rabs, fabsf(a.r[i]));
   pa.npad = npad;
   pa.nclr = nclr;
   pa.clr = clr_base + (size_t)team * T_MAX * nclr;
@@ -978,6 +971,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     const int nown = (T == 1) ? 2 : (w < 2 ? 1 : 0);
     const int chb = (T == 1) ? 0 : w;
     double xi[2] = {0.0, 0.0}, lam[2] = {0.0, 0.0}, cref[2] = {0.0, 0.0};
+    double hreg[2] = {0.0, 0.0};   // h = F^T (F xi1 - g) of the owned channels, lane k: entry k (phase D2)
+    float clkreg = 0.f;            // culling clock of round `lane` (lanes < rounds)
     const float* ini = a.init + l * 3 * NV;
     const float* li = a.lambda_in ? a.lambda_in + l * 5 * NV : nullptr;
 #pragma unroll
@@ -1026,7 +1021,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           // ---- A: xi1 step, Eq. 13/17 via Eq. 4 (fp64) ---------------------
           // every lane runs row min(k, 21) (no divergent branch); lanes >= 22 keep 0
           const int kc = min(k, NV2 - 1);
-          if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * ws->h[ch][k];
+          if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * hreg[c];
           __syncwarp();
           if (c == 0 && lp_pending) lampsi_step();
           {
@@ -1111,9 +1106,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       // residual terms only where they are reported: a compile-time flag keeps the
       // hot (RES = false) copy free of the per-round re-evaluation of a runtime flag
       if (want_res)
-        phase_project<M, true>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, pc);
+        phase_project<M, true>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, hreg, clkreg, pc);
       else
-        phase_project<M, false>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, pc);
+        phase_project<M, false>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, hreg, clkreg, pc);
       __syncwarp();
       BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
@@ -1129,7 +1124,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c >= nown) break;
-          if (k < NV2) lam[c] -= rho * ws->h[chb + c][k];
+          if (k < NV2) lam[c] -= rho * hreg[c];
         }
         if (trace && w == 0 && lane == 0 && active) a.res_trace[l * K + it] = sqrtf(fmaxf(r1sq, 0.f));
       }
@@ -1137,7 +1132,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
 #ifdef BMC_PROFILE
     if (lane == 0 && a.prof)
-      for (int i = 0; i < 12; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * 12 + i] = pc.acc[i];
+      for (int i = 0; i < PROF_SLOTS; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * PROF_SLOTS + i] = pc.acc[i];
 #endif
     __syncwarp();
     if (lp_pending) lampsi_step();   // the last iteration's lambda_psi step
