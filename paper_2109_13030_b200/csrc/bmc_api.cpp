@@ -376,6 +376,24 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
       std::fprintf(stderr, " %.0f", tot / cnt / (pr->iters + 1));
     }
     std::fprintf(stderr, "\n");
+    // spread over teams (instances): loop cycles of a team = max over its warps
+    std::vector<double> tt;
+    for (long long t0 = 0; t0 + team <= nwarps; t0 += team) {
+      double mx = 0.0;
+      for (int wv = 0; wv < team; ++wv) {
+        double tot = 0.0;
+        for (int i = 0; i <= 10; ++i)
+          if (i != 9) tot += (double)hp[(t0 + wv) * 16 + i];
+        mx = std::max(mx, tot);
+      }
+      tt.push_back(mx / (pr->iters + 1));
+    }
+    std::sort(tt.begin(), tt.end());
+    double mean = 0.0;
+    for (double v : tt) mean += v;
+    mean /= std::max<size_t>(1, tt.size());
+    std::fprintf(stderr, "[bmc prof] team loop cycles/iter: mean %.0f p10 %.0f p50 %.0f p90 %.0f p99 %.0f max %.0f\n", mean,
+                 tt[tt.size() / 10], tt[tt.size() / 2], tt[tt.size() * 9 / 10], tt[tt.size() * 99 / 100], tt.back());
   }
   return BMC_OK;
 }

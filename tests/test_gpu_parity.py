@@ -137,6 +137,41 @@ def test_c4_full_batch_sampled_instances():
                   oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr, idx=idx))
 
 
+def test_c5_full_batch_sampled_instances():
+    """C5 at its largest batch (B = 16384, one warp per instance, several waves of
+    CTAs): 10 sampled instances, first and last included, vs the oracle; the best
+    index is the argmin key of the GPU's own outputs."""
+    cfg = CONFIGS["C5"]
+    pr = make_problem(cfg, 2)
+    g = run_gpu(cfg, pr)
+    idx = np.random.default_rng(5).choice(cfg.B, 10, replace=False)
+    idx[0] = 0
+    idx[-1] = cfg.B - 1
+    sub = dict(pr)
+    sub["init"] = pr["init"][idx]
+    r = run_oracle(cfg, sub)
+    gs = {k: g[k][idx] for k in ("coeffs", "cost", "residual")}
+    print(compare(cfg, gs, r, cfg.res_tol, "C5 B=16384 sampled", check_best=False,
+                  oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr, idx=idx))
+    feas = g["residual"][:, 0] <= cfg.res_tol
+    bi = int(g["best"][0])
+    if feas.any():
+        assert feas[bi] and g["cost"][bi] == g["cost"][feas].min()
+        assert bi == int(np.flatnonzero(feas & (g["cost"] == g["cost"][feas].min()))[0])
+
+
+def test_max_obstacles():
+    """n = 160 (the header's maximum, include/bmc.h): several 32-obstacle ballots in
+    the active-list build and the largest shared-memory footprint."""
+    cfg = CONFIGS["C2"].with_(n=160, B=5, K=30)
+    check(cfg, make_problem(cfg, 11), "n=160")
+
+
+def test_single_instance():
+    cfg = CONFIGS["C3"].with_(B=1, K=60)
+    check(cfg, make_problem(cfg, 12), "B=1")
+
+
 def test_large_batch_team_layout_matches_small_batch():
     """The launch shape depends on B (teams of warps for small batches, one warp per
     instance for large ones): an instance's result must not depend on it beyond
