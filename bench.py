@@ -269,6 +269,7 @@ def main():
             kev[i][1].record(stream)
             if xchg is not None:
                 xchg.exchange(out["best"], out["coeffs"], rank * cfg.B)
+                launches += 2   # bmc_pack_best + bmc_select_best (the all-gather is NCCL's)
             ev[i][1].record(stream)
         torch.cuda.synchronize(dev)
         if pg is not None:
@@ -338,7 +339,7 @@ def main():
     peak = fp32_peak(sm_max)
     roof = dict(bound="alu", achieved=achieved / 1e12, peak=peak / 1e12,
                 unit="T FP32 lane-instr/s", frac=achieved / peak, traffic=None,
-                kernel="bmc_am_kernel<3>", algorithmic_ops_per_launch=ops,
+                kernel=f"bmc_am_kernel<{cfg.m}>", algorithmic_ops_per_launch=ops,
                 kernel_ms=1e3 * kern_avg,
                 peak_basis=f"148 SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)")
     if clocks.get("sm_mhz"):
