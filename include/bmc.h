@@ -114,10 +114,14 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out);
 int32_t bmc_solve(bmc_ctx* ctx, const bmc_problem* prob, const bmc_result* res,
                   bmc_stream_t stream);
 
-/* End-to-end solve with HOST pointers (pinned memory recommended): copies the
- * inputs to context-owned device buffers, runs bmc_solve on the context's
- * stream, copies every non-NULL output back, and synchronises.  Same layouts
- * and errors as bmc_solve. */
+/* End-to-end solve with HOST pointers; synchronous.  Same layouts and errors
+ * as bmc_solve.  The obstacle arrays (read by every CTA) and res_trace are
+ * staged through context-owned device buffers (cudaMemcpyAsync on the
+ * context's stream).  Every other array that lies in page-locked host memory
+ * (cudaHostAlloc / cudaHostRegister, e.g. torch pin_memory) is accessed in
+ * place by the kernel: init and lambda_in are read once per instance and the
+ * outputs written once, over PCIe inside this call (no separate copy);
+ * pageable arrays are staged like the obstacles. */
 int32_t bmc_solve_host(bmc_ctx* ctx, const bmc_problem* prob_host, const bmc_result* res_host);
 
 /* ---- multi-GPU best-of-batch exchange ----------------------

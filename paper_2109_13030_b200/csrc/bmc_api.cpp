@@ -446,18 +446,36 @@ int32_t bmc_solve_host(bmc_ctx* c, const bmc_problem* ph, const bmc_result* rh) 
   void* d[10];
   for (int i = 0; i < 10; ++i)
     if ((rc = ensure(c, i, sz[i], &d[i])) != BMC_OK) return rc;
+  // page-locked host arrays are used in place (zero-copy; the kernel reads init /
+  // lambda_in once per instance and writes each output once); the rest is staged
+  auto mapped = [](const void* hp) -> void* {
+    if (!hp) return nullptr;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return (at.type == cudaMemoryTypeHost) ? at.devicePointer : nullptr;
+  };
+  void* m_init = mapped(ph->init);
+  void* m_lam = mapped(ph->lambda_in);
+  void* m_co = mapped(rh->coeffs);
+  void* m_lo = mapped(rh->lambda_out);
+  void* m_res = mapped(rh->residual);
+  void* m_cost = mapped(rh->cost);
+  void* m_best = mapped(rh->best);
   bmc_problem pd = *ph;
   bmc_result rd;
   pd.obs_xy = n ? (const float*)d[0] : nullptr;
   pd.obs_ab = n ? (const float*)d[1] : nullptr;
-  pd.init = (const float*)d[2];
-  pd.lambda_in = ph->lambda_in ? (const float*)d[3] : nullptr;
-  rd.coeffs = (float*)d[4];
-  rd.lambda_out = rh->lambda_out ? (float*)d[5] : nullptr;
-  rd.residual = (float*)d[6];
-  rd.cost = (float*)d[7];
+  pd.init = m_init ? (const float*)m_init : (const float*)d[2];
+  pd.lambda_in = ph->lambda_in ? (m_lam ? (const float*)m_lam : (const float*)d[3]) : nullptr;
+  rd.coeffs = m_co ? (float*)m_co : (float*)d[4];
+  rd.lambda_out = rh->lambda_out ? (m_lo ? (float*)m_lo : (float*)d[5]) : nullptr;
+  rd.residual = m_res ? (float*)m_res : (float*)d[6];
+  rd.cost = m_cost ? (float*)m_cost : (float*)d[7];
   rd.res_trace = rh->res_trace ? (float*)d[8] : nullptr;
-  rd.best = (int64_t*)d[9];
+  rd.best = m_best ? (int64_t*)m_best : (int64_t*)d[9];
   cudaStream_t s = c->hstream;
 #define H2D(dst, src, bytes) \
   if ((bytes) && (e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D")
@@ -467,17 +485,17 @@ int32_t bmc_solve_host(bmc_ctx* c, const bmc_problem* ph, const bmc_result* rh) 
     H2D(d[0], ph->obs_xy, sz[0]);
     H2D(d[1], ph->obs_ab, sz[1]);
   }
-  H2D(d[2], ph->init, sz[2]);
-  if (ph->lambda_in) H2D(d[3], ph->lambda_in, sz[3]);
+  if (!m_init) H2D(d[2], ph->init, sz[2]);
+  if (ph->lambda_in && !m_lam) H2D(d[3], ph->lambda_in, sz[3]);
   rc = solve_impl(c, &pd, &rd, s);
   if (rc != BMC_OK) return rc;
-  D2H(rh->coeffs, d[4], sz[4]);
-  if (rh->lambda_out) D2H(rh->lambda_out, d[5], sz[5]);
-  D2H(rh->residual, d[6], sz[6]);
-  D2H(rh->cost, d[7], sz[7]);
+  if (!m_co) D2H(rh->coeffs, d[4], sz[4]);
+  if (rh->lambda_out && !m_lo) D2H(rh->lambda_out, d[5], sz[5]);
+  if (!m_res) D2H(rh->residual, d[6], sz[6]);
+  if (!m_cost) D2H(rh->cost, d[7], sz[7]);
   const size_t trace_bytes = rh->res_trace ? B * K * 4 : 0;
   D2H(rh->res_trace, d[8], trace_bytes);
-  D2H(rh->best, d[9], 16);
+  if (!m_best) D2H(rh->best, d[9], 16);
 #undef H2D
 #undef D2H
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");

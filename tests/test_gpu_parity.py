@@ -287,6 +287,18 @@ def test_index_base_and_host_path():
     h = s.solve_host(pr["init"], pr["obs_xy"], pr["obs_ab"], pr["bnd"], cfg.K, index_base=1000)
     assert np.array_equal(h["coeffs"], out["coeffs"].cpu().numpy())
     assert np.array_equal(h["best"], best)
+    # page-locked buffers are read / written in place by the kernel (zero-copy):
+    # same bits as the device path, for inputs, outputs and a warm start
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    lam = pin(out["lambda_out"].cpu().numpy())
+    hp = {k: pin(np.full_like(v, np.nan)) for k, v in h.items()}
+    s.solve_host(pin(pr["init"]), pin(pr["obs_xy"]), pin(pr["obs_ab"]), pr["bnd"], cfg.K, index_base=1000,
+                 lambda_in=lam, out=hp)
+    ref = s.solve(_dev(pr["init"]), _dev(pr["obs_xy"]), _dev(pr["obs_ab"]), pr["bnd"], cfg.K, index_base=1000,
+                  lambda_in=_dev(lam))
+    torch.cuda.synchronize()
+    for k in ("coeffs", "lambda_out", "residual", "cost", "best"):
+        assert np.array_equal(hp[k], ref[k].cpu().numpy()), k
 
 
 def test_error_codes():
