@@ -100,6 +100,9 @@ def _ptr(t) -> Optional[int]:
     return t.data_ptr()
 
 
+_OUT_KEYS = ("coeffs", "lambda_out", "residual", "cost", "res_trace", "best")
+
+
 class Solver:
     """bmc_setup / bmc_solve on one device (Python names mirror the C-ABI)."""
 
@@ -120,6 +123,7 @@ class Solver:
         _check(L.bmc_setup(C.byref(self.params), C.byref(h)))
         self._h = h
         self.last_launches = 0
+        self._cache = {}
 
     def close(self):
         if getattr(self, "_h", None):
@@ -129,9 +133,23 @@ class Solver:
     __del__ = close
 
     def _problem(self, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base):
-        bnd = np.asarray(bnd, dtype=np.float64).reshape(18)
-        return BmcProblem(B, index_base, n, iters, (C.c_double * 18)(*bnd), _ptr(obs_xy),
+        bnd = np.ascontiguousarray(bnd, dtype=np.float64).reshape(18)
+        return BmcProblem(B, index_base, n, iters, (C.c_double * 18).from_buffer_copy(bnd), _ptr(obs_xy),
                           _ptr(obs_ab), _ptr(init), _ptr(lambda_in))
+
+    def _marshal(self, slot, arrays, scalars, bnd, build):
+        """ctypes argument structs of the last call per entry point, reused while the
+        same buffer objects (identity; the cache keeps them alive, so their addresses
+        cannot be recycled), scalars and boundary values come back -- the steady
+        state of a bench or MPC loop -- so a repeated call skips the marshalling."""
+        bkey = np.ascontiguousarray(bnd, dtype=np.float64).tobytes()
+        c = self._cache.get(slot)
+        if (c is not None and len(c[0]) == len(arrays) and all(x is y for x, y in zip(c[0], arrays))
+                and c[1] == scalars and c[2] == bkey):
+            return c[3]
+        structs = build()
+        self._cache[slot] = (tuple(arrays), scalars, bkey, structs)
+        return structs
 
     def solve(self, init, obs_xy, obs_ab, bnd, iters: int, lambda_in=None, trace: bool = False,
               index_base: int = 0, out: Optional[dict] = None, stream=None) -> dict:
@@ -140,29 +158,48 @@ class Solver:
         dev = torch.device("cuda", self.device)
         B = int(init.shape[0])
         n = int(obs_xy.shape[0]) if obs_xy is not None else 0
-        for name, t in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
-            if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev):
-                raise ValueError(f"{name} must be a contiguous float32 tensor on {dev}")
-        if out is None:
-            out = dict(
-                coeffs=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
-                lambda_out=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
-                residual=torch.empty((B, 2), dtype=torch.float32, device=dev),
-                cost=torch.empty((B,), dtype=torch.float32, device=dev),
-                best=torch.empty((2,), dtype=torch.int64, device=dev),
-            )
-            if trace and iters > 0:
-                out["res_trace"] = torch.empty((B, iters), dtype=torch.float32, device=dev)
-        prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
-                             lambda_in, index_base)
-        res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
-                        _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+        if out is not None:   # steady state: same buffers as the last call -> cached structs
+            outs = tuple(out.get(k) for k in _OUT_KEYS)
+            arrays = (init, obs_xy, obs_ab, lambda_in) + outs
+            # torch storage can move under the same tensor object (resize_): key on addresses too
+            addrs = tuple(t.data_ptr() if t is not None else 0 for t in arrays)
+            prob, res = self._marshal("dev", arrays, (B, n, iters, index_base) + addrs,
+                                      bnd, lambda: self._dev_structs(dev, B, n, iters, bnd, obs_xy, obs_ab, init,
+                                                                     lambda_in, index_base, out))
+        else:
+            out = self._dev_out(dev, B, iters, trace)
+            prob, res = self._dev_structs(dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
         L = load_library()
         _check(L.bmc_solve(self._h, C.byref(prob), C.byref(res), C.c_void_p(stream.cuda_stream)))
         self.last_launches = L.bmc_last_launch_count(self._h)
         return out
+
+    @staticmethod
+    def _dev_out(dev, B, iters, trace):
+        import torch
+        out = dict(
+            coeffs=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
+            lambda_out=torch.empty((B, 5, NV), dtype=torch.float32, device=dev),
+            residual=torch.empty((B, 2), dtype=torch.float32, device=dev),
+            cost=torch.empty((B,), dtype=torch.float32, device=dev),
+            best=torch.empty((2,), dtype=torch.int64, device=dev),
+        )
+        if trace and iters > 0:
+            out["res_trace"] = torch.empty((B, iters), dtype=torch.float32, device=dev)
+        return out
+
+    def _dev_structs(self, dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out):
+        import torch
+        for name, t in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
+            if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev):
+                raise ValueError(f"{name} must be a contiguous float32 tensor on {dev}")
+        prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
+                             lambda_in, index_base)
+        res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
+                        _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+        return prob, res
 
     def sample_init(self, B: int, bnd, seed: int, stream: int = 0, sigma_x: float = 1.0, sigma_y: float = 5.0,
                     index_base: int = 0, line_first: bool = True, out=None, cuda_stream=None):
@@ -186,19 +223,28 @@ class Solver:
         """End-to-end solve from host arrays (pinned recommended); synchronous."""
         B = int(init.shape[0])
         n = int(obs_xy.shape[0]) if obs_xy is not None else 0
-        for name, a in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
-            if a is not None and (a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]):
-                raise ValueError(f"{name} must be a C-contiguous float32 array")
+
+        def build():
+            for name, a in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
+                if a is not None and (a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]):
+                    raise ValueError(f"{name} must be a C-contiguous float32 array")
+            prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
+                                 lambda_in, index_base)
+            res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
+                            _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+            return prob, res
+
         if out is None:
             out = dict(coeffs=np.empty((B, 5, NV), np.float32), lambda_out=np.empty((B, 5, NV), np.float32),
                        residual=np.empty((B, 2), np.float32), cost=np.empty((B,), np.float32),
                        best=np.empty((2,), np.int64))
             if trace and iters > 0:
                 out["res_trace"] = np.empty((B, iters), np.float32)
-        prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
-                             lambda_in, index_base)
-        res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
-                        _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
+            prob, res = build()
+        else:   # steady state: same buffers as the last call -> cached structs
+            outs = tuple(out.get(k) for k in _OUT_KEYS)
+            prob, res = self._marshal("host", (init, obs_xy, obs_ab, lambda_in) + outs, (B, n, iters, index_base),
+                                      bnd, build)
         L = load_library()
         _check(L.bmc_solve_host(self._h, C.byref(prob), C.byref(res)))
         self.last_launches = L.bmc_last_launch_count(self._h)
