@@ -346,6 +346,9 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   const long long nwarps = ((pr->B + ipc - 1) / ipc) * (long long)ipc * team;
   if (prof && cudaMalloc(&a.prof, sizeof(long long) * 16 * nwarps) == cudaSuccess)
     cudaMemsetAsync(a.prof, 0, sizeof(long long) * 16 * nwarps, s);
+  const long long ngrid = (pr->B + ipc - 1) / ipc;
+  if (prof && cudaMalloc(&a.prof_t, sizeof(long long) * 8 * ngrid) == cudaSuccess)
+    cudaMemsetAsync(a.prof_t, 0, sizeof(long long) * 8 * ngrid, s);
   cudaError_t e = launch_am(a, wpc, s);
   c->last_launches = 1;
   if (e != cudaSuccess) return cuda_fail(e, "bmc_am_kernel launch");
@@ -354,6 +357,29 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
     cudaStreamSynchronize(s);
     cudaMemcpy(hp.data(), a.prof, sizeof(long long) * hp.size(), cudaMemcpyDeviceToHost);
     cudaFree(a.prof);
+    if (a.prof_t) {   // per-CTA wall clock (globaltimer, ns): start spread, prologue, loop, epilogue
+      std::vector<long long> ht(8 * ngrid);
+      cudaMemcpy(ht.data(), a.prof_t, sizeof(long long) * ht.size(), cudaMemcpyDeviceToHost);
+      cudaFree(a.prof_t);
+      long long t0 = ht[0], t3 = ht[3], s_last = ht[0];
+      double seg[6] = {0, 0, 0, 0, 0, 0};   // start->issued, issued->staged, staged->blob, blob->prologue, loop, epilogue
+      for (long long b = 0; b < ngrid; ++b) {
+        const long long* h = &ht[8 * b];
+        t0 = std::min(t0, h[0]);
+        s_last = std::max(s_last, h[0]);
+        t3 = std::max(t3, h[3]);
+        seg[0] += h[4] - h[0];
+        seg[1] += h[5] - h[4];
+        seg[2] += h[6] - h[5];
+        seg[3] += h[1] - h[6];
+        seg[4] += h[7] - h[1];
+        seg[5] += h[3] - h[7];
+      }
+      std::fprintf(stderr, "[bmc prof] CTA wall (us, means): start spread %.2f | staging issued %.2f, staged %.2f, "
+                   "blob wait %.2f, setup %.2f | loop (team 0) %.2f | outputs + argmin %.2f | first start -> last exit %.2f\n",
+                   (s_last - t0) * 1e-3, seg[0] / ngrid * 1e-3, seg[1] / ngrid * 1e-3, seg[2] / ngrid * 1e-3,
+                   seg[3] / ngrid * 1e-3, seg[4] / ngrid * 1e-3, seg[5] / ngrid * 1e-3, (t3 - t0) * 1e-3);
+    }
     const char* names[16] = {"A", "bar1", "B", "bar2", "C", "D2mma", "bar3", "D2+", "E", "tested", "D1", "needed",
                              "D1eval", "D1cull", "D1coll", "D1U+mma"};
     for (int role = 0; role < team; ++role) {

@@ -77,6 +77,7 @@ struct KernelArgs {
   // evaluated in fp32 as deviations from it
   double ref_x0, ref_dx, ref_y0, ref_dy;
   long long* prof;             // [warps][12] phase cycles (PROFILE builds only) or null
+  long long* prof_t;           // [grid][4] globaltimer stamps per CTA (PROFILE builds only) or null
   int no_cull;                 // testing aid (BMC_NOCULL): every obstacle tested every round
   int blockdiag;               // M, K11 block diagonal (symmetric footprint, sum r_i = 0)
 };

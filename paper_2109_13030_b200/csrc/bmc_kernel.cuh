@@ -125,7 +125,17 @@ struct PhaseClock {
     if ((i) >= 0) (pc).acc[i] += t1_ - (pc).s0; \
     (pc).s0 = t1_;                       \
   } while (0)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BMC_STAMP(i) \
+  do {                                                                       \
+    if (threadIdx.x == 0 && a.prof_t) a.prof_t[(long long)blockIdx.x * 8 + (i)] = gtimer(); \
+  } while (0)
 #else
+#define BMC_STAMP(i) ((void)0)
 struct PhaseClock {};
 #define BMC_TICK(pc, i) ((void)0)
 #define BMC_SUB(pc, i) ((void)0)
@@ -861,6 +871,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (TT > 1 ? (size_t)wpc * HP_SLOTS : 0));
   uint64_t* tbar = mbar + 1;   // [ipc] hand-off barriers
 
+  BMC_STAMP(0);   // CTA start
   // --- stage the batch-invariant data -------------------------------------
   if (tid == 0) mbar_init(mbar, 1);
   if (tid < ipc) mbar_init(tbar + tid, 1);
@@ -904,8 +915,11 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
   for (int i = tid; i < ipc * (3 * QP + 2 * T_MAX); i += blockDim.x)
     (&wsbase[i / (3 * QP + 2 * T_MAX)].pxy[0].x)[i % (3 * QP + 2 * T_MAX)] = 0.f;
+  BMC_STAMP(4);   // staging loops issued (thread 0)
   const bool all_circ = __syncthreads_and(circ);
+  BMC_STAMP(5);   // staging done
   mbar_wait(mbar, 0);
+  BMC_STAMP(6);   // blob landed
   __syncthreads();
   if (tid < 32) dm_table(ub + DM_TAB, tid, a.T);
   if (tid < NV2) {   // u = K12 b per channel (boundary part of Eq. 4)
@@ -923,6 +937,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
   }
   __syncthreads();
+  BMC_STAMP(1);   // prologue done
 
   Proj pa;
   pa.Pt = Pt;
@@ -1135,6 +1150,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       for (int i = 0; i < PROF_SLOTS; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * PROF_SLOTS + i] = pc.acc[i];
 #endif
     __syncwarp();
+    BMC_STAMP(7);   // thread 0's team left the iteration loop
     if (lp_pending) lampsi_step();   // the last iteration's lambda_psi step
     // ---- outputs ----------------------------------------------------------------
     if (active) {
@@ -1193,6 +1209,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   }
   // ---- grid-wide argmin: the last CTA publishes and resets the workspace ----
   __syncthreads();
+  BMC_STAMP(2);   // every team done (outputs written)
   if (tid == 0) {
     __threadfence();
     const unsigned ticket = atomicAdd(a.ws_count, 1u);
@@ -1204,6 +1221,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       atomicExch(a.ws_count, 0u);
     }
   }
+  BMC_STAMP(3);   // CTA exit
 }
 
 }  // namespace
