@@ -221,7 +221,7 @@ def main():
 
     import torch
     from paper_2109_13030_b200 import solver_for
-    from paper_2109_13030_b200.distributed import BestExchange
+    from paper_2109_13030_b200.distributed import BestExchange, solve_sharded, solve_sharded_host
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -244,9 +244,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out)
-        if xchg is not None:
-            xchg.exchange(out["best"], out["coeffs"], rank * cfg.B)
+        solve_sharded(solver, xchg, init, obs, ab, glob["bnd"], cfg.K, rank * cfg.B, out=out)
 
     for _ in range(args.warmup):
         step()
@@ -270,7 +268,7 @@ def main():
             if xchg is not None:
                 xchg.exchange(out["best"], out["coeffs"], rank * cfg.B)
                 launches += 2   # bmc_pack_best + bmc_select_best (the all-gather is NCCL's)
-            ev[i][1].record(stream)
+            ev[i][1].record(stream)   # solve + exchange = solve_sharded (kernel timed separately by kev)
         torch.cuda.synchronize(dev)
         if pg is not None:
             torch.distributed.barrier()
@@ -307,12 +305,22 @@ def main():
     h_out = dict(coeffs=pin(np.empty((B, 5, 11), np.float32)), lambda_out=pin(np.empty((B, 5, 11), np.float32)),
                  residual=pin(np.empty((B, 2), np.float32)), cost=pin(np.empty((B,), np.float32)),
                  best=pin(np.empty((2,), np.int64)))
+    # the user's call: the shard's solve from host buffers plus, for N > 1, the
+    # best-of-batch exchange and the read-back of the global best (16 B + 220 B)
+    g_best, g_coeffs = pin(np.empty(2, np.int64)), pin(np.empty(55, np.float32))
+
+    def e2e_step():
+        solve_sharded_host(solver, xchg, h_init, h_obs, h_ab, glob["bnd"], cfg.K, rank * cfg.B, out=h_out,
+                           best_host=g_best, coeffs_host=g_coeffs)
+
     for _ in range(args.warmup):
-        solver.solve_host(h_init, h_obs, h_ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=h_out)
+        e2e_step()
+    if pg is not None:
+        torch.distributed.barrier()
     e2e_t = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        solver.solve_host(h_init, h_obs, h_ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=h_out)
+        e2e_step()
         e2e_t.append(time.perf_counter() - t0)
     t_e2e = sum(e2e_t)
     if pg is not None:
@@ -321,7 +329,7 @@ def main():
         t_e2e = float(tt[0])
     e2e_value = world * cfg.B * cfg.K * args.steps / t_e2e
     h2d = h_init.nbytes + h_obs.nbytes + h_ab.nbytes
-    d2h = sum(v.nbytes for v in h_out.values())
+    d2h = sum(v.nbytes for v in h_out.values()) + (g_best.nbytes + g_coeffs.nbytes if world > 1 else 0)
 
     if rank != 0:
         if pg is not None:

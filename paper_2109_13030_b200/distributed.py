@@ -14,6 +14,8 @@ from __future__ import annotations
 import ctypes as C
 from typing import Callable, Optional
 
+import numpy as np
+
 from .bmc import _check, load_library
 
 RECORD_WORDS = 32
@@ -67,3 +69,46 @@ def shard_bounds(global_batch: int, world: int, rank: int):
     per = -(-global_batch // world)
     start = min(rank * per, global_batch)
     return start, max(0, min(per, global_batch - start))
+
+
+def solve_sharded(solver, xchg: Optional[BestExchange], init, obs_xy, obs_ab, bnd, iters: int, index_base: int,
+                  lambda_in=None, out: Optional[dict] = None):
+    """One rank's part of a batch solve sharded over a process group (SURVEY.md
+    §3 call stack 3): bmc_solve on this rank's shard (device tensors, current
+    stream), then the best-of-batch exchange.  Returns (shard outputs, global
+    best [2], best coefficients [55]); with xchg None (one rank) the shard's own
+    best.  Asynchronous on the current stream like Solver.solve."""
+    out = solver.solve(init, obs_xy, obs_ab, bnd, iters, lambda_in=lambda_in, index_base=index_base, out=out)
+    if xchg is None:
+        return out, out["best"], None
+    best, coeffs = xchg.exchange(out["best"], out["coeffs"], index_base)
+    return out, best, coeffs
+
+
+def solve_sharded_host(solver, xchg: Optional[BestExchange], init, obs_xy, obs_ab, bnd, iters: int,
+                       index_base: int, out: dict, lambda_in=None, best_host=None, coeffs_host=None):
+    """End-to-end variant from host buffers: bmc_solve_host on the shard (page-locked
+    buffers are accessed in place), then -- for more than one rank -- the exchange
+    reads the shard's best and coefficients from those page-locked output buffers
+    (mapped into the device address space) and the global best (16 B) and its
+    coefficients (220 B) are copied back into `best_host` / `coeffs_host`.
+    Synchronous.  Returns (out, best_host, coeffs_host)."""
+    import torch
+    solver.solve_host(init, obs_xy, obs_ab, bnd, iters, lambda_in=lambda_in, index_base=index_base, out=out)
+    if xchg is None:
+        return out, out["best"], None
+    dev = torch.device(xchg.device)
+    best_t = torch.from_numpy(out["best"])
+    coeffs_t = torch.from_numpy(out["coeffs"])
+    if dev.type == "cuda" and not (best_t.is_pinned() and coeffs_t.is_pinned()):
+        best_t, coeffs_t = best_t.to(dev), coeffs_t.to(dev)   # pageable outputs: staged on the device
+    best, coeffs = xchg.exchange(best_t, coeffs_t, index_base)
+    if best_host is None:
+        best_host = np.empty(2, np.int64)
+    if coeffs_host is None:
+        coeffs_host = np.empty(55, np.float32)
+    torch.from_numpy(best_host).copy_(best, non_blocking=True)
+    torch.from_numpy(coeffs_host).copy_(coeffs, non_blocking=True)
+    if dev.type == "cuda":
+        torch.cuda.current_stream(dev).synchronize()
+    return out, best_host, coeffs_host

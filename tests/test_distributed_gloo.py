@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2109_13030_b200.distributed import RECORD_WORDS, BestExchange, shard_bounds
+from paper_2109_13030_b200.distributed import RECORD_WORDS, BestExchange, shard_bounds, solve_sharded_host
 
 
 def _free_port():
@@ -44,6 +44,18 @@ def host_select(records, nranks, best_out, coeffs_out):
     coeffs_out.copy_(r[i, 1:].clone().view(torch.float32)[:55])
 
 
+class _FakeSolver:
+    """Stands in for Solver.solve_host: writes a fixed shard result into `out`."""
+
+    def __init__(self, best, coeffs):
+        self.best, self.coeffs = best, coeffs
+
+    def solve_host(self, init, obs_xy, obs_ab, bnd, iters, lambda_in=None, index_base=0, out=None):
+        out["best"][...] = self.best
+        out["coeffs"][...] = self.coeffs
+        return out
+
+
 def _key(infeasible, value, gidx):
     bits = int(np.array([value], dtype=np.float32).view(np.uint32)[0])
     return (infeasible << 62) | (bits << 30) | gidx
@@ -67,6 +79,11 @@ def _worker(rank, world, port, scenario, out):
         x = BestExchange(dist.group.WORLD, torch.device("cpu"), pack=host_pack, select=host_select)
         gb, gc = x.exchange(best, coeffs, start)
         out[rank] = (int(gb[0]), int(gb[1]), float(gc[0]), float(gc[54]))
+        # the same exchange through the end-to-end entry point (host buffers)
+        solver = _FakeSolver(best.numpy(), coeffs.numpy())
+        res = dict(best=np.empty(2, np.int64), coeffs=np.empty((size, 5, 11), np.float32))
+        _, hb, hc = solve_sharded_host(solver, x, None, None, None, None, 1, start, out=res)
+        assert (int(hb[0]), int(hb[1]), float(hc[0]), float(hc[54])) == out[rank]
     finally:
         dist.destroy_process_group()
 

@@ -54,3 +54,43 @@ def test_pack_select_equals_global_argmin():
         assert torch.equal(o["coeffs"], whole["coeffs"][r * B:(r + 1) * B])
     assert int(best[0]) == int(whole["best"][0]) and int(best[1]) == int(whole["best"][1])
     assert torch.equal(coeffs, whole["coeffs"][int(best[0])].reshape(-1))
+
+
+def test_sharded_entry_points_single_rank_nccl():
+    """solve_sharded / solve_sharded_host over a one-rank NCCL group: the exchange
+    reads the shard's best from device outputs and, on the host path, from
+    page-locked host outputs mapped into the device address space."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2109_13030_b200 import solver_for
+    from paper_2109_13030_b200.distributed import BestExchange, solve_sharded, solve_sharded_host
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        cfg = CONFIGS["C2"].with_(B=40, K=20)
+        pr = make_problem(cfg, 3)
+        s = solver_for(cfg, device=0)
+        x = BestExchange(dist.group.WORLD, dev)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        out, best, coeffs = solve_sharded(s, x, d(pr["init"]), d(pr["obs_xy"]), d(pr["obs_ab"]), pr["bnd"], cfg.K,
+                                          index_base=500)
+        torch.cuda.synchronize()
+        b = int(best[0])
+        assert 500 <= b < 540 and int(best[1]) == int(out["best"][1])
+        assert torch.equal(coeffs, out["coeffs"][b - 500].reshape(-1))
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        h = {k: pin(np.empty(tuple(v.shape), np.float32 if v.dtype == torch.float32 else np.int64))
+             for k, v in out.items()}
+        _, hb, hc = solve_sharded_host(s, x, pin(pr["init"]), pin(pr["obs_xy"]), pin(pr["obs_ab"]), pr["bnd"], cfg.K,
+                                       500, out=h)
+        assert np.array_equal(hb, best.cpu().numpy()) and np.array_equal(hc, coeffs.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
