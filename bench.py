@@ -132,7 +132,7 @@ def run_reference(args, cfg, rank, world):
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = args.steps * sample * cfg.K / tot
-    line = dict(impl="reference", metric=METRIC, value=value, unit="trajectories*iterations/s",
+    line = dict(impl="reference", metric=metric_name(cfg), value=value, unit="trajectories*iterations/s",
                 n_gpus=world, steps=args.steps, warmup=args.warmup,
                 ms_per_step=1e3 * tot / args.steps, higher_is_better=True, scaling="weak", vs_baseline=None,
                 dtype="f64", data="synthetic",
@@ -144,7 +144,8 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
-METRIC = "trajectories*iterations/s (batch solve: 1000 instances/GPU x 100 AM iterations)"
+def metric_name(cfg) -> str:
+    return f"trajectories*iterations/s (batch solve: {cfg.B} instances/GPU x {cfg.K} AM iterations)"
 
 
 def run_mpc(args, cfg):
@@ -358,7 +359,7 @@ def main():
             roof["traffic"] = json.load(open(traffic_file)).get(f"{cfg.name}_bytes_per_launch")
         except Exception:
             pass
-    line = dict(metric=METRIC, value=value, unit="trajectories*iterations/s", n_gpus=world, steps=args.steps,
+    line = dict(metric=metric_name(cfg), value=value, unit="trajectories*iterations/s", n_gpus=world, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * t_dev / args.steps, higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype="f32 (fp64 KKT steps)", data="synthetic",
                 config=workload(cfg, world), clocks=clocks, gpu_launches=launches,
