@@ -49,10 +49,6 @@ constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per
 constexpr int QP64 = QP + 4;     // row stride of the fp64 basis (BlobLayout::p64_stride)
 constexpr int QPU = QP + 4;      // row stride of WarpSmem::U
 constexpr int HP_SLOTS = 8 * 12; // per-warp partial contractions (D2), doubles
-#ifndef BMC_HANDOFF_STEPS
-#define BMC_HANDOFF_STEPS 8
-#endif
-constexpr int HANDOFF_STEPS = BMC_HANDOFF_STEPS;   // MMA steps of round 0 that warp 0 takes (T = 2)
 
 // Per-instance state shared by the TT warps of its team (per-warp arrays sized
 // by the compile-time team size: shared memory bounds the instances per SM for
@@ -150,14 +146,14 @@ __host__ __device__ inline int clr_stride(int n) { return pad_obstacles(n) + JB;
 // Layout after the constant blob: obstacles [npad + 1][QP] (row npad: the far
 // dummy), abi [npad + 1], u = K12 b, WarpSmem[ipc], clearance stamps
 // [ipc][4][nclr], active lists [ipc * T][nclr], D2 partials [ipc * T][HP_SLOTS],
-// mbarriers (blob copy; one per team for the round-0 hand-off).
+// the mbarrier of the blob copy.
 __host__ __device__ inline size_t smem_bytes(int n, int ipc, int T) {
   const int np = pad_obstacles(n) + 1;
   return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
          U_DOUBLES * sizeof(double) + (size_t)ipc * ws_bytes(T) +
          (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) +
          (T > 1 ? (size_t)ipc * T * HP_SLOTS * sizeof(double) : 0) +
-         16 + (size_t)ipc * 8;
+         16;
 }
 
 // ---------------------------------------------------------------- PTX helpers
@@ -404,8 +400,6 @@ struct Proj {
   double* hp;            // smem D2 partials of the team's warps, [T][HP_SLOTS]
   const double* dmtab;   // smem weights of Dm, Dm^T (dm_table)
   bool no_cull;          // testing aid: test every obstacle (KernelArgs::no_cull)
-  bool handoff;          // T = 2 with a tail round: warp 0 contracts warp 1's round 0
-  uint64_t* tbar;        // the team's hand-off mbarrier
 };
 
 // --------------------------------------------------- collision projections
@@ -597,7 +591,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
 template <int M, bool RES, class WarpSmem>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
-                                              int lane, int w, int T, int team, unsigned hand_phase, double (&hreg)[2],
+                                              int lane, int w, int T, int team, double (&hreg)[2],
                                               float& clkreg, PhaseClock& pc) {
   const int q = pa.q, n = pa.n;
   const float* __restrict__ Pt = pa.Pt;
@@ -617,7 +611,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   const float* __restrict__ ucol = &ws->U[lane >> 2][lane & 3];   // B fragment: U[k = lane % 4][n = lane / 4]
   // two accumulator sets (even / odd MMA steps): dependent chains of 4, not 8
   double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
-  auto contract_round = [&](int u, int s0, int s1) {   // MMA steps [s0, s1) of a full round
+  auto contract_round = [&](int u) {
     const int t0 = 32 * u;
     const float* __restrict__ up = ucol + t0;
     const double* __restrict__ a0 = P64 + aoff0 + t0;
@@ -625,7 +619,6 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     if (t0 + 32 <= q) {   // full round: 8 steps, immediate offsets
 #pragma unroll
       for (int st = 0; st < 8; ++st) {
-        if (st < s0 || st >= s1) continue;
         const double b = f2d(up[4 * st]);
         if (st & 1) {
           mma_f64_884(e0, a0[4 * st], b);
@@ -645,10 +638,6 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       }
     }
   };
-  // T = 2 with a tail round: warp 1 projects rounds 0, 2 and warp 0 rounds 1 and the
-  // tail, so warp 0 also contracts round 0 (after warp 1 signals its U on the team's
-  // mbarrier) -- the MMAs leave the critical warp
-  const bool give = pa.handoff && w == 1, take = pa.handoff && w == 0;
 #pragma unroll 1
   for (int u = T - 1 - w; u < pa.rounds; u += T) {   // this warp's rounds (leader: the lightest)
     // samples t >= q of the last round have a zero basis row and far-away
@@ -774,17 +763,8 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       rps = fmaf(dth, dth, rps);
     }
     __syncwarp();   // the round's U is complete
-    if (give && u == 0) {
-      if (lane == 0) mbar_arrive(pa.tbar);
-      contract_round(0, 0, 8 - HANDOFF_STEPS);
-    } else {
-      contract_round(u, 0, 8);
-    }
+    contract_round(u);
     BMC_SUB(pc, 15);   // U and the round's MMAs
-  }
-  if (take) {
-    mbar_wait(pa.tbar, hand_phase);
-    contract_round(0, 8 - HANDOFF_STEPS, 8);
   }
   __syncwarp();
   BMC_TICK(pc, 10);
@@ -864,17 +844,36 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
   constexpr int T = TT;                              // warps per instance (compile time: folds the
   const int ipc = wpc / T;                           // team bookkeeping), instances per CTA
-  const int team = warp / T, w = warp - team * T;    // instance slot in the CTA, rank in the team
+  // instance slot in the CTA and rank in its team.  Warp i runs on SMSP i % 4.
+  // Teams of 2 straddle the scheduler pairs: in every group of 4 warps, warps
+  // (0, 2) and (1, 3) form the teams, so rank 0 (rounds 1, 3: one round plus
+  // the tail at q = 100) sits on SMSP 0 or 1 and rank 1 (rounds 0, 2) on SMSP 2
+  // or 3; a trailing pair (wpc % 4 == 2) forms one team on SMSPs 0 and 1.  With
+  // 7 teams (C3) SMSPs 0 and 1 hold 4 warps and 2 and 3 hold 3: the light ranks
+  // go where the schedulers are busiest (C3 0.623 -> 0.592 ms).
+  int team_, w_;
+  if (T == 2) {
+    const int g = warp >> 2, rr = warp & 3;
+    if (4 * g + 3 < wpc) {
+      team_ = 2 * g + (rr & 1);
+      w_ = rr >> 1;
+    } else {
+      team_ = 2 * g;
+      w_ = rr;
+    }
+  } else {
+    team_ = warp / T;
+    w_ = warp - team_ * T;
+  }
+  const int team = team_, w = w_;
   float* clr_base = reinterpret_cast<float*>(wsbase + ipc);
   int* list_base = reinterpret_cast<int*>(clr_base + (size_t)ipc * T_MAX * nclr);
   double* hp_base = reinterpret_cast<double*>(list_base + (size_t)wpc * nclr);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(hp_base + (TT > 1 ? (size_t)wpc * HP_SLOTS : 0));
-  uint64_t* tbar = mbar + 1;   // [ipc] hand-off barriers
 
   BMC_STAMP(0);   // CTA start
   // --- stage the batch-invariant data -------------------------------------
   if (tid == 0) mbar_init(mbar, 1);
-  if (tid < ipc) mbar_init(tbar + tid, 1);
   __syncthreads();
   const unsigned blob_bytes = (unsigned)BlobLayout::bytes(QP);
   if (tid == 0) {
@@ -961,12 +960,6 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.hp = (TT > 1) ? hp_base + (size_t)team * T * HP_SLOTS : reinterpret_cast<double*>(&wsbase[team].U[0][0]);
   pa.dmtab = ub + DM_TAB;
   pa.no_cull = a.no_cull != 0;
-  // hand-off when warp 0's second round is a light tail: T = 2, an even number of
-  // rounds, a partial last round, and a moderate collision load (n m <= 128; with
-  // more obstacle pairs the tail round itself is busy -- measured: C3 (90) gains
-  // 2.7 %, C4 (200) would lose 3 %).  Deterministic for a given launch.
-  pa.handoff = (T == 2) && (pa.rounds % 2 == 0) && (q % 32 != 0) && (n * M <= 128);
-  pa.tbar = tbar + team;
   float r[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) r[i] = a.r[i];
@@ -1121,9 +1114,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       // residual terms only where they are reported: a compile-time flag keeps the
       // hot (RES = false) copy free of the per-round re-evaluation of a runtime flag
       if (want_res)
-        phase_project<M, true>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, hreg, clkreg, pc);
+        phase_project<M, true>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
       else
-        phase_project<M, false>(pa, r, ws, lane, w, T, team, (unsigned)(it + 1) & 1u, hreg, clkreg, pc);
+        phase_project<M, false>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
       __syncwarp();
       BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
@@ -1147,7 +1140,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
 #ifdef BMC_PROFILE
     if (lane == 0 && a.prof)
-      for (int i = 0; i < PROF_SLOTS; ++i) a.prof[((long long)blockIdx.x * wpc + warp) * PROF_SLOTS + i] = pc.acc[i];
+      for (int i = 0; i < PROF_SLOTS; ++i)   // logical order (team, rank): the host analysis groups by it
+        a.prof[((long long)blockIdx.x * wpc + team * T + w) * PROF_SLOTS + i] = pc.acc[i];
 #endif
     __syncwarp();
     BMC_STAMP(7);   // thread 0's team left the iteration loop
