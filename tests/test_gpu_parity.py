@@ -160,6 +160,34 @@ def test_c5_full_batch_sampled_instances():
         assert bi == int(np.flatnonzero(feas & (g["cost"] == g["cost"][feas].min()))[0])
 
 
+@pytest.mark.parametrize("B", [888, 1184])
+def test_team_mapping_even_team_count(B):
+    """Teams of 2 are formed across the scheduler pairs (bmc_kernel.cuh): B = 888 and
+    1184 give 6 and 8 teams per CTA (whole groups of 4 warps, no trailing pair;
+    B = 1000 with its trailing pair is covered above).  Sampled instances vs the
+    oracle, and the same rows from a launch with one warp per instance."""
+    import os
+    cfg = CONFIGS["C3"].with_(B=B, K=40)
+    pr = make_problem(cfg, 5)
+    g = run_gpu(cfg, pr)
+    idx = np.random.default_rng(B).choice(B, 10, replace=False)
+    idx[-1] = B - 1
+    sub = dict(pr)
+    sub["init"] = pr["init"][idx]
+    r = run_oracle(cfg, sub)
+    gs = {k: g[k][idx] for k in ("coeffs", "cost", "residual")}
+    print(compare(cfg, gs, r, cfg.res_tol, f"B={B} teams of 2", check_best=False,
+                  oracle=Oracle(oracle_params(cfg), cfg.n), problem=pr, idx=idx))
+    os.environ["BMC_TEAM"] = "1"
+    try:
+        g1 = run_gpu(cfg, pr)
+    finally:
+        del os.environ["BMC_TEAM"]
+    print(compare(cfg, {k: g1[k][idx] for k in ("coeffs", "cost", "residual")}, r, cfg.res_tol,
+                  f"B={B} one warp per instance", check_best=False, oracle=Oracle(oracle_params(cfg), cfg.n),
+                  problem=pr, idx=idx))
+
+
 def test_max_obstacles():
     """n = 160 (the header's maximum, include/bmc.h): several 32-obstacle ballots in
     the active-list build and the largest shared-memory footprint."""
