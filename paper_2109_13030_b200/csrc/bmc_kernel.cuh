@@ -429,6 +429,7 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
                                               float* __restrict__ clr, float A, int lane, const float2 (&XY)[M],
                                               const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
                                               float& rc) {
+  bool zero = false;
 #pragma unroll 1
   for (int jb = 0; jb < na; jb += JB) {
     float r2m[JB];
@@ -452,7 +453,7 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
       }
       r2m[jj] = r2min;
     }
-    unsigned qm = 0u;
+    unsigned qm = 1u;
 #pragma unroll
     for (int jj = 0; jj < JB; ++jj) {
       // round minimum (non-negative floats order as their bit patterns)
@@ -463,8 +464,9 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
       const int j = list[jb + lane];
       clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
     }
+    zero |= (qm == 0u);   // a circle centre exactly on an obstacle centre (G18)
   }
-  return na > 0 ? 1u : 0u;
+  return __any_sync(FULL, zero) ? 1u : 0u;
 }
 
 // Any obstacle kinds, one obstacle at a time.  GUARD handles x~ = y~ = 0
@@ -697,12 +699,13 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     float rc = 0.f;
     const float2* ob = pa.obs + t;
     BMC_SUB(pc, 12);   // evaluation, velocity / acceleration, heading
-    // circular obstacles: culled, blocked inside test (coll_circ); ellipses:
-    // the plain loop.  A non-finite result (x~ = y~ = 0 exactly, G18, rare)
-    // reruns the plain loop with the guard; one call site keeps the hot loop
-    // small in the instruction cache.
+    // circular obstacles: culled closed forms (coll_circ); ellipses: the plain
+    // loop.  x~ = y~ = 0 exactly (G18, rare: detected by the stamp reductions
+    // for circles, by a non-finite sum for ellipses) reruns the round with the
+    // guarded plain loop; one call site keeps the hot loop small in the
+    // instruction cache.
     bool general = !pa.all_circ;
-    bool exact = general;   // warp-uniform: some closed form ran (only those can be non-finite)
+    bool rerun = false;   // warp-uniform: x~ = y~ = 0 exactly somewhere -> guarded pass (G18)
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
       const float clk0 = __shfl_sync(FULL, clkreg, u);
@@ -721,22 +724,25 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       pc.acc[9] += na;
 #endif
       BMC_SUB(pc, 13);   // culling clock and active list
-      exact = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
+      // the exact zero shows up in the stamp reductions (a round minimum r2 of 0)
+      rerun = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
     }
     bool guard = false;
 #pragma unroll 1
-    for (;;) {
-      if (general) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
-      if (guard || !exact) break;
-      float chk = rc;
+    for (;;) {   // one call site of the plain loop: ellipses, and the rare guarded rerun
+      if (general || guard) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
+      if (guard) break;
+      if (general) {   // ellipses: a non-finite sum flags the exact zero
+        float chk = rc;
 #pragma unroll
-      for (int i = 0; i < M; ++i) chk += D[i].x + D[i].y;
-      if (!__any_sync(FULL, !isfinite(chk))) break;
+        for (int i = 0; i < M; ++i) chk += D[i].x + D[i].y;
+        rerun = __any_sync(FULL, !isfinite(chk));
+      }
+      if (!rerun) break;
 #pragma unroll
       for (int i = 0; i < M; ++i) D[i] = make_float2(0.f, 0.f);
       rc = 0.f;
       guard = true;
-      general = true;
     }
     BMC_SUB(pc, 14);   // collision projections
     float2 nDs = make_float2(0.f, 0.f), nE = nDs;   // -sum_i delta_i, -sum_i r_i delta_i
