@@ -43,7 +43,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int QP = Q_MAX;   // sample stride of every per-sample smem array
-constexpr int JB = 4;       // obstacles per inside-test block
+constexpr int JB = 4;       // obstacles per collision block (coll_circ)
 
 constexpr int T_MAX = QP / 32;   // warps per instance ("team"): at most one per round
 constexpr int QP64 = QP + 4;     // row stride of the fp64 basis (BlobLayout::p64_stride)
@@ -423,6 +423,51 @@ struct Proj {
 // steps per obstacle and the same result bits).  The pass records, per
 // visited obstacle, the round's clearance min over samples and circles of
 // |centre - o_j| - a_j, stamped with the movement clock A.
+// NB obstacles of the active list (one basic block: their loads and MUFU
+// latencies overlap), then the warp reductions of their stamps.  Returns true
+// in some lane if a circle centre sits exactly on an obstacle centre (G18).
+template <int M, int NB>
+__device__ __forceinline__ bool coll_block(const bool RES, const float2* __restrict__ ob,
+                                           const float4* __restrict__ abi, const int* __restrict__ list, int jb,
+                                           float* __restrict__ clr, float A, int lane, const float2 (&XY)[M],
+                                           const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
+                                           float& rc) {
+  float r2m[NB];
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    const int j = list[jb + jj];
+    const float2 o = ob[j * QP];
+    const float a = abi[j].x;
+    float r2min = INFINITY;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const float2 tt = sub2(XY[i], o);   // (x~, y~)
+      const float r2 = fmaf(tt.y, tt.y, tt.x * tt.x);
+      const float sc = fmaxf(fmaf(a, rsqrt_ftz(r2), -1.f), 0.f);
+      const float2 dd = mul2(bc2(sc), tt);
+      D[i] = add2(D[i], dd);
+      if (RES) rc = fmaf(dd.x, dd.x - 2.f * rec[i], fmaf(dd.y, dd.y - 2.f * res_s[i], rc));
+      r2min = fminf(r2min, r2);
+    }
+    r2m[jj] = r2min;
+  }
+  unsigned qm = 1u;
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) {
+    // round minimum (non-negative floats order as their bit patterns)
+    const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(r2m[jj]));
+    qm = (lane == jj) ? mn : qm;
+  }
+  if (lane < NB) {
+    const int j = list[jb + lane];
+    clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
+  }
+  return qm == 0u;
+}
+
+// The active list in blocks of JB obstacles, then a block of 2 and one of 1
+// for the remainder: most rounds have one or two active obstacles, and padding
+// them to a block of 4 with far dummies cost 1-3 % (C3, C4).
 template <int M>
 __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __restrict__ ob,
                                               const float4* __restrict__ abi, const int* __restrict__ list, int na,
@@ -430,42 +475,15 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
                                               const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
                                               float& rc) {
   bool zero = false;
+  int jb = 0;
 #pragma unroll 1
-  for (int jb = 0; jb < na; jb += JB) {
-    float r2m[JB];
-    // the JB closed forms first (one basic block: their loads and MUFU latencies
-    // overlap), the warp reductions of the stamps after them
-#pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int j = list[jb + jj];   // the list is padded to a multiple of JB with a far dummy
-      const float2 o = ob[j * QP];
-      const float a = abi[j].x;
-      float r2min = INFINITY;
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const float2 tt = sub2(XY[i], o);   // (x~, y~)
-        const float r2 = fmaf(tt.y, tt.y, tt.x * tt.x);
-        const float sc = fmaxf(fmaf(a, rsqrt_ftz(r2), -1.f), 0.f);
-        const float2 dd = mul2(bc2(sc), tt);
-        D[i] = add2(D[i], dd);
-        if (RES) rc = fmaf(dd.x, dd.x - 2.f * rec[i], fmaf(dd.y, dd.y - 2.f * res_s[i], rc));
-        r2min = fminf(r2min, r2);
-      }
-      r2m[jj] = r2min;
-    }
-    unsigned qm = 1u;
-#pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      // round minimum (non-negative floats order as their bit patterns)
-      const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(r2m[jj]));
-      qm = (lane == jj) ? mn : qm;
-    }
-    if (lane < JB) {
-      const int j = list[jb + lane];
-      clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
-    }
-    zero |= (qm == 0u);   // a circle centre exactly on an obstacle centre (G18)
+  for (; jb + JB <= na; jb += JB)
+    zero |= coll_block<M, JB>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
+  if (jb + 2 <= na) {
+    zero |= coll_block<M, 2>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
+    jb += 2;
   }
+  if (jb < na) zero |= coll_block<M, 1>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
   return __any_sync(FULL, zero) ? 1u : 0u;
 }
 
@@ -521,8 +539,7 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
 constexpr float CULL_MARGIN = 2e-3f;
 
 // Active list of one round: obstacles whose clearance no longer covers the
-// movement since it was stamped, padded to a multiple of JB with the far dummy
-// `npad`.  Returns the padded length.
+// movement since it was stamped.  Returns its length.
 __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* __restrict__ list, int npad,
                                             float lim, int lane) {
   int na = 0;
@@ -541,10 +558,8 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
       na += __popc(bal);
     }
   }
-  const int nap = (na + JB - 1) & ~(JB - 1);
-  if (lane < nap - na) list[na + lane] = npad;
   __syncwarp();
-  return nap;
+  return na;
 }
 
 // ---------------------------------------------------------------- phase B
