@@ -1042,42 +1042,52 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 #endif
 #pragma unroll 1
     for (int it = -1; it < K; ++it) {
+      // ---- A: xi1 step, Eq. 13/17 via Eq. 4 (fp64), for the owned channels --------
+      // (both channels for T = 1: their mat-vecs are independent and interleave)
+      double vnew[2] = {0.0, 0.0};
+      if (it >= 0) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c >= nown) break;
+          if (k < NV2) ws->rhs[chb + c][k] = lam[c] - rho * hreg[c];
+        }
+        __syncwarp();
+        if (nown > 0 && lp_pending) lampsi_step();
+        // every lane runs row min(k, 21) (no divergent branch); lanes >= 22 keep 0
+        const int kc = min(k, NV2 - 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c >= nown) break;
+          const int ch = chb + c;
+          // 8 independent fp64 chains (depth <= 6): the step is latency-bound.  With a
+          // symmetric footprint M and K11 are block diagonal (setup.cpp): row k only
+          // meets the columns of its own block (c_x rows 0..10, c_c rows 11..21).
+          double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+          if (a.blockdiag) {
+            const int j0 = (kc < NV) ? 0 : NV;
+#pragma unroll
+            for (int jj = 0; jj < NV; ++jj) {
+              const int j = j0 + jj;
+              acc[jj & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[jj & 3]);
+              acc[4 + (jj & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (jj & 3)]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < NV2; ++j) {
+              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
+              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
+            }
+          }
+          const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+          vnew[c] = (k < NV2) ? v : 0.0;
+        }
+        __syncwarp();   // every lane has read xi1 and rhs
+      }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         if (c >= nown) break;
         const int ch = chb + c;
-        if (it >= 0) {
-          // ---- A: xi1 step, Eq. 13/17 via Eq. 4 (fp64) ---------------------
-          // every lane runs row min(k, 21) (no divergent branch); lanes >= 22 keep 0
-          const int kc = min(k, NV2 - 1);
-          if (k < NV2) ws->rhs[ch][k] = lam[c] - rho * hreg[c];
-          __syncwarp();
-          if (c == 0 && lp_pending) lampsi_step();
-          {
-            // 8 independent fp64 chains (depth <= 6): the step is latency-bound.  With a
-            // symmetric footprint M and K11 are block diagonal (setup.cpp): row k only
-            // meets the columns of its own block (c_x rows 0..10, c_c rows 11..21).
-            double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            if (a.blockdiag) {
-              const int j0 = (kc < NV) ? 0 : NV;
-#pragma unroll
-              for (int jj = 0; jj < NV; ++jj) {
-                const int j = j0 + jj;
-                acc[jj & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[jj & 3]);
-                acc[4 + (jj & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (jj & 3)]);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < NV2; ++j) {
-                acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
-                acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
-              }
-            }
-            const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-            xi[c] = (k < NV2) ? v : 0.0;
-          }
-          __syncwarp();
-        }
+        if (it >= 0) xi[c] = vnew[c];
         {
           // position (deviation from the boundary line), Dm c and Dm^2 c in fp64
           // (Dm tridiagonal: (Dm c)_k = (-k c_{k-1} + (2k - n) c_k + (n - k) c_{k+1}) / T,
