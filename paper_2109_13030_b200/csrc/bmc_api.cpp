@@ -274,7 +274,12 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   const int rounds = (c->q + 31) / 32;
   int wmax = 16;   // resident warps per SM at the kernel's register budget
   if (const char* s = std::getenv("BMC_WMAX")) wmax = std::max(1, std::min(32, std::atoi(s)));
-  int ipc = (int)std::min<int64_t>(wmax, (pr->B + dev_sms - 1) / dev_sms);
+  // batches beyond one wave of wmax instances per SM: as many CTA waves as
+  // needed at wmax, then the fewest instances per CTA that still fit in them
+  // (B = 4096: 2 waves of 14 instead of 1.73 waves of 16 -- every wave costs
+  // the same time, and fewer warps per SM run each wave faster)
+  const int64_t waves = std::max<int64_t>(1, (pr->B + (int64_t)dev_sms * wmax - 1) / ((int64_t)dev_sms * wmax));
+  int ipc = (int)std::min<int64_t>(wmax, (pr->B + dev_sms * waves - 1) / (dev_sms * waves));
   int team = std::max(1, std::min(rounds, wmax / std::max(1, ipc)));
   if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
   if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
