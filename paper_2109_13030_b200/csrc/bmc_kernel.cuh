@@ -9,6 +9,8 @@
 // Time samples are processed in rounds of 32 lanes (t = 32 u + lane); warp w
 // of a team takes rounds u = T-1-w, 2T-1-w, ...  Samples t >= q of the last
 // round have a zero basis row and far-away obstacle slots and drop out.
+// Teams of 2 are formed across the SMSP pairs (warps (0, 2) and (1, 3) of
+// every group of 4), which balances the four schedulers at 7 teams per CTA.
 //
 // Per iteration (paper step order):
 //   A  xi1 step (Eq. 13/17 via Eq. 4):  xi1' = M xi1 + K11 (lambda - rho h) + K12 b
