@@ -285,7 +285,9 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
   if (team < 1 || team > 4) team = 1;
   if (team == 3) team = (ipc * 4 <= wmax) ? 4 : 2;   // kernels exist for teams of 1, 2, 4
-  if (ipc < 1 || ipc * team > 16) ipc = std::max(1, 16 / team);   // <= 512 threads (__launch_bounds__)
+  int wcta = 16;   // warps per CTA (__launch_bounds__(512)); BMC_WCTA: register-capped experiment builds
+  if (const char* s = std::getenv("BMC_WCTA")) wcta = std::max(1, std::min(32, std::atoi(s)));
+  if (ipc < 1 || ipc * team > wcta) ipc = std::max(1, wcta / team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024) --ipc;
   if (kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024)
     return fail(BMC_EINVAL, "n_obs * q too large for shared memory");
