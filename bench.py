@@ -103,8 +103,9 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(cfg, pr, sample: int, iters: int):
-    """The fp64 oracle, as it stands, on this host's cores (bounded sample)."""
+def cpu_baseline(cfg, pr, sample: int, iters: int, sample_1t: int = 0):
+    """The fp64 oracle, as it stands, on this host's cores (bounded sample), and
+    with sample_1t > 0 also on one core (all cores and 1 core)."""
     from oracle import Oracle, OracleParams
     o = Oracle(OracleParams(q=cfg.q, T=cfg.T, degree=cfg.degree, r=cfg.offsets, v_max=cfg.v_max,
                             a_max=cfg.a_max, rho=cfg.rho, rho_psi=cfg.rho_psi, res_tol=cfg.res_tol), cfg.n)
@@ -112,9 +113,16 @@ def cpu_baseline(cfg, pr, sample: int, iters: int):
     t0 = time.perf_counter()
     o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"][:sample], iters, nthreads=cores)
     dt = time.perf_counter() - t0
-    return dict(value=sample * iters / dt, unit="trajectories*iterations/s", cores=cores, kind="oracle",
-                sample=f"{sample} instances x {iters} iterations of the {cfg.name} scene "
-                       f"(fp64 C oracle, OpenMP over instances), {dt:.2f} s wall")
+    cb = dict(value=sample * iters / dt, unit="trajectories*iterations/s", cores=cores, kind="oracle",
+              sample=f"{sample} instances x {iters} iterations of the {cfg.name} scene "
+                     f"(fp64 C oracle, OpenMP over instances), {dt:.2f} s wall")
+    if sample_1t > 0:
+        t0 = time.perf_counter()
+        o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"][:sample_1t], iters, nthreads=1)
+        dt1 = time.perf_counter() - t0
+        cb["one_core"] = dict(value=sample_1t * iters / dt1, unit="trajectories*iterations/s", cores=1,
+                              sample=f"{sample_1t} instances x {iters} iterations, {dt1:.2f} s wall")
+    return cb
 
 
 def run_reference(args, cfg, rank, world):
@@ -182,11 +190,29 @@ def run_mpc(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def workload(cfg, world):
-    return {"workload": f"{cfg.name}: batch {cfg.B}/GPU, horizon {cfg.q}, {cfg.m} circles, {cfg.n} "
+def workload(cfg, world, global_batch=None):
+    gb = cfg.B * world if global_batch is None else global_batch
+    per = cfg.B if global_batch is None else -(-global_batch // world)
+    kind = "batch {}/GPU".format(per) if global_batch is None else "batch {} split over {} GPU(s)".format(gb, world)
+    return {"workload": f"{cfg.name}: {kind}, horizon {cfg.q}, {cfg.m} circles, {cfg.n} "
                         f"{'dynamic' if cfg.dynamic else 'static'} obstacles, {cfg.K} AM iterations",
-            "batch_per_gpu": cfg.B, "global_batch": cfg.B * world, "q": cfg.q, "m": cfg.m, "n_obs": cfg.n,
+            "batch_per_gpu": per, "global_batch": gb, "q": cfg.q, "m": cfg.m, "n_obs": cfg.n,
             "iters": cfg.K, "l2": "flushed between steps (256 MiB memset, outside the timed events)"}
+
+
+def required_work(cfg):
+    """Required-work accounting from the PROFILE build's count of the (round, obstacle)
+    pairs the culled collision loop actually evaluates (profiles/required_work.json,
+    tools/required_work.py): the fixed per-sample work plus 32 lanes x m circles x 8 FP32
+    instructions per evaluated pair, per instance-iteration."""
+    path = os.path.join(ROOT, "profiles", "required_work.json")
+    try:
+        rw = json.load(open(path)).get(cfg.name)
+    except Exception:
+        return None
+    if not rw or rw.get("q") != cfg.q or rw.get("m") != cfg.m or rw.get("n") != cfg.n:
+        return None
+    return float(cfg.q) * (99 + 99 + 20 + 6 * cfg.m) + rw["evaluated_pairs_per_instance_iter"] * 32 * 8 * cfg.m, rw
 
 
 def main():
@@ -200,9 +226,13 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=16)
     ap.add_argument("--cpu-sample", type=int, default=960,
                     help="oracle instances for cpu_baseline (about 10-30 s on a 16-core host)")
+    ap.add_argument("--cpu-sample-1t", type=int, default=32,
+                    help="oracle instances for the one-core cpu_baseline column (about 5-10 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mpc", action="store_true",
                     help="NEXT-1: time the receding-horizon MPC tick (P:585) instead of the C3 batch solve")
+    ap.add_argument("--strong", type=int, default=0, metavar="B",
+                    help="strong scaling: one global batch of B instances split over the GPUs (e.g. 16384, C5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -212,6 +242,10 @@ def main():
     cfg = CONFIGS[args.config]
     if args.batch:
         cfg = cfg.with_(B=args.batch)
+    global_batch = None
+    if args.strong:   # total work fixed: rank r solves instances [r per, (r+1) per) of args.strong
+        global_batch = args.strong
+        cfg = cfg.with_(B=-(-args.strong // world))
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
@@ -232,20 +266,26 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist.group.WORLD
     # every rank builds the same scene from the seed; rank r owns instances [r B, (r+1) B)
-    glob = make_problem(cfg, 0, B=cfg.B * world)
-    shard = slice(rank * cfg.B, (rank + 1) * cfg.B)
+    n_glob = cfg.B * world if global_batch is None else global_batch
+    glob = make_problem(cfg, 0, B=n_glob)
+    shard = slice(min(rank * cfg.B, n_glob), min((rank + 1) * cfg.B, n_glob))
     init_h = np.ascontiguousarray(glob["init"][shard])
+    B_rank = init_h.shape[0]
+    assert B_rank > 0, "every rank needs a non-empty shard to time"
     init = torch.from_numpy(init_h).to(dev)
     obs = torch.from_numpy(glob["obs_xy"]).to(dev)
     ab = torch.from_numpy(glob["obs_ab"]).to(dev)
     solver = solver_for(cfg, device=local)
+    # the team size of the whole batch on one GPU: every instance is bitwise the
+    # unsharded solve's, whatever N (include/bmc.h "Determinism")
+    team = solver.team_for(n_glob)
     xchg = BestExchange(pg, dev) if world > 1 else None
-    out = solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B)
+    out = solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, team=team)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        solve_sharded(solver, xchg, init, obs, ab, glob["bnd"], cfg.K, rank * cfg.B, out=out)
+        solve_sharded(solver, xchg, init, obs, ab, glob["bnd"], cfg.K, rank * cfg.B, out=out, team=team)
 
     for _ in range(args.warmup):
         step()
@@ -263,7 +303,7 @@ def main():
             flush.zero_()
             ev[i][0].record(stream)
             kev[i][0].record(stream)
-            solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out)
+            solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out, team=team)
             launches += solver.last_launches
             kev[i][1].record(stream)
             if xchg is not None:
@@ -282,7 +322,7 @@ def main():
             t_end = time.perf_counter() + 1.5
             while time.perf_counter() < t_end:   # kernel only: no collective in the soak
                 for _ in range(20):
-                    solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out)
+                    solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, out=out, team=team)
                 torch.cuda.synchronize(dev)
         clocks = clk2.summary()
         clocks["clock_window"] = "soak (same step, 1.5 s, right after the timed region)"
@@ -297,12 +337,12 @@ def main():
         t_dev, t_kern = float(tt[0]), float(tt[1])
     else:
         t_kern = sum(kern_ms) / 1e3
-    value = world * cfg.B * cfg.K * args.steps / t_dev
+    value = n_glob * cfg.K * args.steps / t_dev
 
     # ---- end to end through the host-buffer C-ABI (bmc_solve_host) ------------
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     h_init, h_obs, h_ab = pin(init_h), pin(glob["obs_xy"]), pin(glob["obs_ab"])
-    B = cfg.B
+    B = B_rank
     h_out = dict(coeffs=pin(np.empty((B, 5, 11), np.float32)), lambda_out=pin(np.empty((B, 5, 11), np.float32)),
                  residual=pin(np.empty((B, 2), np.float32)), cost=pin(np.empty((B,), np.float32)),
                  best=pin(np.empty((2,), np.int64)))
@@ -312,7 +352,7 @@ def main():
 
     def e2e_step():
         solve_sharded_host(solver, xchg, h_init, h_obs, h_ab, glob["bnd"], cfg.K, rank * cfg.B, out=h_out,
-                           best_host=g_best, coeffs_host=g_coeffs)
+                           best_host=g_best, coeffs_host=g_coeffs, team=team)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -328,7 +368,7 @@ def main():
         tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_e2e = float(tt[0])
-    e2e_value = world * cfg.B * cfg.K * args.steps / t_e2e
+    e2e_value = n_glob * cfg.K * args.steps / t_e2e
     h2d = h_init.nbytes + h_obs.nbytes + h_ab.nbytes
     d2h = sum(v.nbytes for v in h_out.values()) + (g_best.nbytes + g_coeffs.nbytes if world > 1 else 0)
 
@@ -342,7 +382,7 @@ def main():
     except Exception:
         pass
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    ops = algorithmic_fp32_ops(cfg.q, cfg.m, cfg.n) * cfg.B * cfg.K      # per launch
+    ops = algorithmic_fp32_ops(cfg.q, cfg.m, cfg.n) * B_rank * cfg.K      # per launch (rank 0's shard)
     kern_avg = t_kern / args.steps
     achieved = ops / kern_avg
     peak = fp32_peak(sm_max)
@@ -353,21 +393,35 @@ def main():
                 peak_basis=f"148 SM x 128 FP32 lanes x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)")
     if clocks.get("sm_mhz"):
         roof["frac_at_observed_clock"] = achieved / fp32_peak(clocks["sm_mhz"])
+    # DRAM bytes per launch and issue activity of the current kernel: one ncu --set full
+    # capture of this bench's launch (profiles/dram_traffic.json, written by tools/ncu_summary.py)
     traffic_file = os.path.join(ROOT, "profiles", "dram_traffic.json")
-    if os.path.exists(traffic_file):
+    if os.path.exists(traffic_file) and global_batch is None:
         try:
-            roof["traffic"] = json.load(open(traffic_file)).get(f"{cfg.name}_bytes_per_launch")
+            tj = json.load(open(traffic_file))
+            roof["traffic"] = tj.get(f"{cfg.name}_bytes_per_launch")
+            roof["traffic_source"] = tj.get("source")
+            if tj.get(f"{cfg.name}_issue_active_pct") is not None:
+                roof["issue_active_pct"] = tj[f"{cfg.name}_issue_active_pct"]
         except Exception:
             pass
+    rw = required_work(cfg)
+    if rw is not None:   # the work the culled kernel must do, next to the method's algorithmic count
+        req_ops = rw[0] * B_rank * cfg.K
+        roof["required_ops_per_launch"] = req_ops
+        roof["required_frac"] = req_ops / kern_avg / peak
+        roof["required_basis"] = rw[1].get("source")
     line = dict(metric=metric_name(cfg), value=value, unit="trajectories*iterations/s", n_gpus=world, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * t_dev / args.steps, higher_is_better=True,
-                scaling="weak", vs_baseline=None, dtype="f32 (fp64 KKT steps)", data="synthetic",
-                config=workload(cfg, world), clocks=clocks, gpu_launches=launches,
+                scaling="weak" if global_batch is None else "strong", vs_baseline=None,
+                dtype="f32 (fp64 KKT steps)", data="synthetic",
+                config=workload(cfg, world, global_batch) | {"team": team}, clocks=clocks, gpu_launches=launches,
                 e2e=dict(value=e2e_value, unit="trajectories*iterations/s", h2d_bytes_per_step=int(h2d),
                          d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * t_e2e / args.steps),
                 roofline=roof, wall_s=wall)
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg, glob, args.cpu_sample, cfg.K)
+        line["cpu_baseline"] = cpu_baseline(cfg, glob, min(args.cpu_sample, n_glob), cfg.K,
+                                            sample_1t=min(args.cpu_sample_1t, n_glob))
     print(json.dumps(line), flush=True)
     if pg is not None:
         torch.distributed.destroy_process_group()

@@ -30,7 +30,13 @@
  *
  * Threading / streams: every function is re-entrant across contexts.  Calls
  * of bmc_solve on ONE context must be ordered on one stream (they share the
- * context's argmin workspace).  bmc_last_error() is thread-local.
+ * context's argmin workspace); bmc_solve_host has a workspace of its own and
+ * may overlap them.  bmc_last_error() is thread-local.
+ *
+ * Determinism: an instance's outputs depend on its own inputs, the context and
+ * the team size (warps per instance, bmc_problem.team) -- never on B, on its
+ * position in the batch, on index_base or on the other instances.  With a
+ * fixed team a sharded solve reproduces the unsharded one bit for bit.
  */
 #ifndef BMC_H
 #define BMC_H
@@ -83,6 +89,10 @@ typedef struct {
   const float* obs_ab;     /* [n][2] effective (inflated) semi-axes a_j, b_j > 0 (G13)   */
   const float* init;       /* [B][3][11] initial Bernstein coefficients c_x, c_y, c_psi  */
   const float* lambda_in;  /* [B][5][11] warm-start multipliers (lambda, lambda_psi) or NULL */
+  int32_t team;            /* warps per instance: 1, 2 or 4; 0 = chosen from B (bmc_team_for).
+                              The fp64 partial sums of an instance are combined in warp
+                              order, so its output bits depend on the team size: pass the
+                              team of the whole batch when solving shards of it. */
 } bmc_problem;
 
 /* Outputs.  Layouts are row-major fp32 (int64 for best). */
@@ -128,17 +138,23 @@ int32_t bmc_solve_host(bmc_ctx* ctx, const bmc_problem* prob_host, const bmc_res
  * A batch sharded over ranks (bmc_problem.index_base = first global index of
  * the shard) has one global argmin: the minimum packed key over all ranks.
  * Record layout (BMC_RECORD_WORDS int64 per rank, device memory):
- *   word 0 = packed key, words 1.. = the 55 fp32 coefficients of that
- *   instance (c_x, c_c, c_y, c_s, c_psi), zero padded.
- * bmc_pack_best writes this rank's record from the `best` and `coeffs` of a
- * finished bmc_solve (stream-ordered after it); the caller all-gathers the
+ *   word 0 = packed key, words 1.. = as fp32: the 55 coefficients of that
+ *   instance (c_x, c_c, c_y, c_s, c_psi), then its residuals r1, r_psi and its
+ *   cost J (floats 55..57; zero when `residual` / `cost` are NULL), zero padded.
+ * bmc_pack_best writes this rank's record from the `best`, `coeffs` and
+ * (optionally) `residual` and `cost` of a finished bmc_solve (stream-ordered
+ * after it) -- on one GPU this is also the device-side gather of the best
+ * instance's outputs into one 256-byte block; the caller all-gathers the
  * records (e.g. NCCL all_gather over NVLink); bmc_select_best picks the
  * minimum key and writes best_out[2] = {global index, key} and
- * coeffs_out[55].  Both are one-warp kernels on `stream`.  Errors:
- * BMC_EINVAL (NULL pointer, nranks < 1), BMC_ECUDA (launch failure). */
+ * coeffs_out[55] (the coefficients; the whole record is in `records`).  Both are one-warp kernels on `stream`.  A rank with an
+ * empty shard contributes best = {0, -1} (key ~0: never the minimum unless
+ * every rank is empty); bmc_pack_best then reads no coefficients.  Errors:
+ * BMC_EINVAL (NULL pointer, nranks < 1), BMC_ECUDA (launch failure); both
+ * set bmc_last_error(). */
 #define BMC_RECORD_WORDS 32
-int32_t bmc_pack_best(const int64_t* best, const float* coeffs, int64_t index_base, int64_t* record,
-                      bmc_stream_t stream);
+int32_t bmc_pack_best(const int64_t* best, const float* coeffs, const float* residual, const float* cost,
+                      int64_t index_base, int64_t* record, bmc_stream_t stream);
 int32_t bmc_select_best(const int64_t* records, int32_t nranks, int64_t* best_out, float* coeffs_out,
                         bmc_stream_t stream);
 
@@ -168,6 +184,10 @@ typedef struct {
   int32_t line_first;
 } bmc_sample_params;
 int32_t bmc_sample_init(bmc_ctx* ctx, const bmc_sample_params* sp, float* init, bmc_stream_t stream);
+
+/* The team size (warps per instance) bmc_solve picks for a batch of B
+ * instances with team = 0 on this context's device: 1, 2 or 4; 0 if B < 1. */
+int32_t bmc_team_for(const bmc_ctx* ctx, int64_t B);
 
 /* Kernel launches issued by the last bmc_solve / bmc_solve_host on ctx. */
 int32_t bmc_last_launch_count(const bmc_ctx* ctx);

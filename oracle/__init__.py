@@ -47,6 +47,8 @@ class _Params(C.Structure):
         ("alpha_rule", C.c_int),
         ("lampsi_printed_sign", C.c_int),
         ("res_tol", C.c_double),
+        ("fp32_model", C.c_int),
+        ("noise_seed", C.c_ulonglong),
     ]
 
 
@@ -126,13 +128,16 @@ class OracleParams:
     alpha_rule: int = 0
     lampsi_printed_sign: int = 0
     res_tol: float = 1e-2
+    fp32_model: int = 0          # parity harness: fp32 rounding model (oracle.h)
+    noise_seed: int = 0          # 0: round to nearest; else stochastic rounding keyed by this seed
     _r: np.ndarray = field(default=None, repr=False)
 
     def to_c(self) -> _Params:
         self._r = _f64(self.r)
         return _Params(self.q, self.T, self.degree, len(self._r), _ptr(self._r), self.v_max,
                        self.a_max, self.rho, self.rho_psi, self.w_copy, self.boundary_mask,
-                       self.alpha_rule, self.lampsi_printed_sign, self.res_tol)
+                       self.alpha_rule, self.lampsi_printed_sign, self.res_tol, self.fp32_model,
+                       self.noise_seed)
 
 
 def basis(q: int, T: float, degree: int):

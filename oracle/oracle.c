@@ -46,6 +46,7 @@ struct or_ctx {
   int n, nv, q, m, nb, R, rows, cols;
   int bsel[6];
   double *P, *Pd, *Pdd; /* [q][nv] */
+  double *P32, *Pd32, *Pdd32; /* fp32 model only: the basis rounded to fp32 */
   double* A;            /* [nb][nv] */
   double* F;            /* [rows][cols] */
   double* Qbar;         /* [cols][cols] */
@@ -152,6 +153,9 @@ void or_destroy(or_ctx* c) {
   free(c->P);
   free(c->Pd);
   free(c->Pdd);
+  free(c->P32);
+  free(c->Pd32);
+  free(c->Pdd32);
   free(c->A);
   free(c->F);
   free(c->Qbar);
@@ -174,7 +178,8 @@ or_ctx* or_create(const or_params* p, int n_obs, int* err) {
   or_ctx* c = NULL;
   if (!p || p->degree < 2 || p->q < p->degree + 1 || !(p->T > 0.0) || p->m < 1 || !p->r ||
       n_obs < 0 || !(p->rho > 0.0) || !(p->rho_psi > 0.0) || !(p->v_max > 0.0) ||
-      !(p->a_max > 0.0) || p->w_copy < 0.0 || (p->boundary_mask & ~0x3Fu)) {
+      !(p->a_max > 0.0) || p->w_copy < 0.0 || (p->boundary_mask & ~0x3Fu) ||
+      (p->fp32_model && p->degree + 1 > 32)) {
     e = OR_EINVAL;
     goto fail;
   }
@@ -199,6 +204,16 @@ or_ctx* or_create(const or_params* p, int n_obs, int* err) {
   c->Pd = (double*)malloc(sizeof(double) * (size_t)q * nv);
   c->Pdd = (double*)malloc(sizeof(double) * (size_t)q * nv);
   or_basis(q, p->T, p->degree, c->P, c->Pd, c->Pdd);
+  if (p->fp32_model) { /* fp32 model: the evaluation basis is held in fp32 */
+    c->P32 = (double*)malloc(sizeof(double) * (size_t)q * nv);
+    c->Pd32 = (double*)malloc(sizeof(double) * (size_t)q * nv);
+    c->Pdd32 = (double*)malloc(sizeof(double) * (size_t)q * nv);
+    for (int i = 0; i < q * nv; ++i) {
+      c->P32[i] = (double)(float)c->P[i];
+      c->Pd32[i] = (double)(float)c->Pd[i];
+      c->Pdd32[i] = (double)(float)c->Pdd[i];
+    }
+  }
 
   /* boundary rows A: "first and last rows of P and its derivatives" (G11) */
   c->nb = 0;
@@ -469,6 +484,128 @@ static void heading_target(const or_ctx* c, const traj_t* tr) {
     tr->theta[t] = (tr->ss[t] == 0.0 && tr->cc[t] == 0.0) ? 0.0 : atan2(tr->ss[t], tr->cc[t]);
 }
 
+/* ------------------------------------------------ fp32 rounding model
+ * (or_params.fp32_model; parity harness only).
+ * The same iteration as above, with each quantity that the product path holds
+ * in fp32 rounded where it is formed; everything else (the KKT steps, P^T theta,
+ * F^T of the residual rows, lambda, J) stays fp64 as it is there.  Sites:
+ *   evaluation: coefficients (positions relative to the boundary line, the
+ *     frame the product path keeps positions in), the fp32 basis, and every
+ *     evaluated sample x, y, xdot, ydot, xddot, yddot, psi, c, s;
+ *   cos psi, sin psi, theta = atan2(s, c);
+ *   obstacle positions relative to the boundary line (once, to nearest);
+ *   circle centres, (x~, y~), and every projection offset delta = g - v;
+ *   the copy residuals e = c - cos psi.
+ * The residual rows then read (F xi1 - g) = r_i e - delta (collision),
+ * -delta (velocity, acceleration), e (copy), i.e. g is rebuilt around the
+ * fp64 rows of F xi1 from the rounded offsets. */
+typedef struct {
+  const or_ctx* c;
+  unsigned long long seed; /* 0: round to nearest */
+  long long inst;
+  int it;
+  double xr0, xrd, yr0, yrd; /* boundary line: x_ref(tau) = xr0 + xrd tau, tau = t/(q-1) */
+} r32_t;
+
+static unsigned long long mix64(unsigned long long z) { /* splitmix64 finaliser */
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* v rounded to fp32: to nearest, or stochastically (probability of rounding
+ * up = distance to the lower neighbour / spacing) when the model is seeded. */
+static double r32(const r32_t* z, int site, long long idx, double v) {
+  const float f = (float)v;
+  if (!z->seed || !isfinite(v) || !isfinite(f) || (double)f == v) return (double)f;
+  float lo = f, hi = f;
+  if ((double)f < v)
+    hi = nextafterf(f, INFINITY);
+  else
+    lo = nextafterf(f, -INFINITY);
+  const double p = (v - (double)lo) / ((double)hi - (double)lo);
+  unsigned long long h = mix64(z->seed);
+  h = mix64(h ^ (unsigned long long)z->inst);
+  h = mix64(h ^ ((unsigned long long)(z->it + 2) << 40) ^ ((unsigned long long)site << 32) ^
+            (unsigned long long)idx);
+  const double u = (double)(h >> 11) * 0x1.0p-53;
+  return u < p ? (double)hi : (double)lo;
+}
+
+/* sum_k B[t][k] coef_k rounded (the coefficients rounded first) */
+static double eval32(const r32_t* z, int site, const double* B, int t, const double* coef) {
+  const int nv = z->c->nv;
+  double s = 0.0;
+  for (int k = 0; k < nv; ++k) s += B[t * nv + k] * coef[k];
+  return r32(z, site, t, s);
+}
+
+/* theta from the fp32 copies (model counterpart of heading_target) */
+static void heading_target32(const r32_t* z, const double* xi1, traj_t* tr) {
+  const or_ctx* c = z->c;
+  const int q = c->q, nv = c->nv;
+  double cc[32], ss[32];
+  for (int k = 0; k < nv; ++k) {
+    cc[k] = r32(z, 1, k, xi1[1 * nv + k]);
+    ss[k] = r32(z, 2, k, xi1[3 * nv + k]);
+  }
+  for (int t = 0; t < q; ++t) {
+    const double c32 = eval32(z, 3, c->P32, t, cc), s32 = eval32(z, 4, c->P32, t, ss);
+    tr->theta[t] = (s32 == 0.0 && c32 == 0.0) ? 0.0 : r32(z, 5, t, atan2(s32, c32));
+  }
+}
+
+/* g of Eq. 10-11 in the model (counterpart of build_g); tr holds the fp64 samples */
+static void build_g32(const r32_t* z, const double* xi1, const double* xi2, const traj_t* tr,
+                      const double* obs_xy, const double* obs_ab, double* g) {
+  const or_ctx* c = z->c;
+  const int q = c->q, m = c->m, n = c->n, R = c->R, nv = c->nv;
+  double cx[32], cy[32], cc[32], ss[32], cp[32];
+  for (int k = 0; k < nv; ++k) { /* Bernstein control points of the line: xr0 + xrd k / degree */
+    cx[k] = r32(z, 10, k, xi1[0 * nv + k] - (z->xr0 + z->xrd * (double)k / (double)(nv - 1)));
+    cy[k] = r32(z, 11, k, xi1[2 * nv + k] - (z->yr0 + z->yrd * (double)k / (double)(nv - 1)));
+    cc[k] = r32(z, 12, k, xi1[1 * nv + k]);
+    ss[k] = r32(z, 13, k, xi1[3 * nv + k]);
+    cp[k] = r32(z, 14, k, xi2[k]);
+  }
+  for (int t = 0; t < q; ++t) {
+    const double tau = (double)t / (double)(q - 1);
+    const double xr = z->xr0 + z->xrd * tau, yr = z->yr0 + z->yrd * tau;
+    const double x32 = eval32(z, 20, c->P32, t, cx), y32 = eval32(z, 21, c->P32, t, cy);
+    const double xd = r32(z, 22, t, tr->xd[t]), yd = r32(z, 23, t, tr->yd[t]);
+    const double xdd = r32(z, 24, t, tr->xdd[t]), ydd = r32(z, 25, t, tr->ydd[t]);
+    const double psi = eval32(z, 26, c->P32, t, cp);
+    const double c32 = eval32(z, 27, c->P32, t, cc), s32 = eval32(z, 28, c->P32, t, ss);
+    const double cps = r32(z, 29, t, cos(psi)), sps = r32(z, 30, t, sin(psi));
+    const double ec = r32(z, 31, t, c32 - cps), es = r32(z, 32, t, s32 - sps);
+    double al, d;
+    or_project_bound(xd, yd, c->p.v_max, &al, &d); /* offsets delta = g - v */
+    g[t] = tr->xd[t] + r32(z, 33, t, d * c->p.v_max * cos(al) - xd);
+    g[R + t] = tr->yd[t] + r32(z, 34, t, d * c->p.v_max * sin(al) - yd);
+    or_project_bound(xdd, ydd, c->p.a_max, &al, &d);
+    g[q + t] = tr->xdd[t] + r32(z, 35, t, d * c->p.a_max * cos(al) - xdd);
+    g[R + q + t] = tr->ydd[t] + r32(z, 36, t, d * c->p.a_max * sin(al) - ydd);
+    g[row_copy(c, t)] = tr->cc[t] - ec;
+    g[R + row_copy(c, t)] = tr->ss[t] - es;
+    for (int j = 0; j < n; ++j) {
+      const double a = obs_ab[2 * j], b = obs_ab[2 * j + 1];
+      const double ox = (double)(float)(obs_xy[(size_t)j * 2 * q + t] - xr);  /* once, to nearest */
+      const double oy = (double)(float)(obs_xy[(size_t)j * 2 * q + q + t] - yr);
+      for (int i = 0; i < m; ++i) {
+        const long long id = ((long long)j * m + i) * q + t;
+        const double X = r32(z, 40, id, x32 + c->r[i] * cps), Y = r32(z, 41, id, y32 + c->r[i] * sps);
+        const double xt = r32(z, 42, id, X - ox), yt = r32(z, 43, id, Y - oy);
+        or_project_obstacle(xt, yt, a, b, c->p.alpha_rule, &al, &d);
+        const double dx = r32(z, 44, id, a * d * cos(al) - xt), dy = r32(z, 45, id, b * d * sin(al) - yt);
+        /* residual row (x + r_i c) - g = r_i e - delta */
+        g[row_coll(c, j, i, t)] = tr->x[t] + c->r[i] * tr->cc[t] - c->r[i] * ec + dx;
+        g[R + row_coll(c, j, i, t)] = tr->y[t] + c->r[i] * tr->ss[t] - c->r[i] * es + dy;
+      }
+    }
+  }
+}
+
 static long long pack_key(double r1, double J, double tau, long long gidx) {
   int infeasible = !(r1 <= tau);
   const double v = infeasible ? r1 : J;
@@ -489,9 +626,9 @@ typedef struct {
   double *xi1_tr, *xi2_tr, *lam_tr, *g_tr, *theta_tr, *r1_tr, *rpsi_tr;
 } inst_out;
 
-static int run_instance(const or_ctx* c, int K, const double* bnd, const double* obs_xy,
-                        const double* obs_ab, const double* init, const double* lam_in,
-                        inst_out* o) {
+static int run_instance(const or_ctx* c, int K, long long gidx, const double* bnd,
+                        const double* obs_xy, const double* obs_ab, const double* init,
+                        const double* lam_in, inst_out* o) {
   const int q = c->q, nv = c->nv, cols = c->cols, rows = c->rows;
   const double rho = c->p.rho, rho_psi = c->p.rho_psi;
   double* buf = (double*)calloc((size_t)(3 * cols + 4 * nv + 2 * rows + 10 * q), sizeof(double));
@@ -527,9 +664,31 @@ static int run_instance(const or_ctx* c, int K, const double* bnd, const double*
   }
   for (int a = 0; a < cols; ++a) lam[a] = lam_in ? lam_in[a] : 0.0;
   for (int k = 0; k < nv; ++k) lampsi[k] = lam_in ? lam_in[cols + k] : 0.0;
+  /* fp32 rounding model (off for the oracle proper): positions are held
+   * relative to the boundary line p(0) -> p(T), else p(0), else p(T), else 0 */
+  r32_t z;
+  memset(&z, 0, sizeof(z));
+  z.c = c;
+  z.seed = c->p.noise_seed;
+  z.inst = gidx;
+  z.it = -1;
+  {
+    const unsigned mk = c->p.boundary_mask;
+    const int h0 = (mk & 1u) != 0, hT = (mk & 8u) != 0;
+    z.xr0 = h0 ? bnd[0] : (hT ? bnd[3] : 0.0);
+    z.yr0 = h0 ? bnd[6] : (hT ? bnd[9] : 0.0);
+    z.xrd = (h0 && hT) ? bnd[3] - bnd[0] : 0.0;
+    z.yrd = (h0 && hT) ? bnd[9] - bnd[6] : 0.0;
+  }
+  const int model = c->p.fp32_model != 0;
   eval_traj(c, xi1, xi2, &tr);
-  heading_target(c, &tr);
-  build_g(c, &tr, obs_xy, obs_ab, g);
+  if (model) {
+    heading_target32(&z, xi1, &tr);
+    build_g32(&z, xi1, xi2, &tr, obs_xy, obs_ab, g);
+  } else {
+    heading_target(c, &tr);
+    build_g(c, &tr, obs_xy, obs_ab, g);
+  }
 
 #define RECORD(kk)                                                                  \
   do {                                                                              \
@@ -561,16 +720,23 @@ static int run_instance(const or_ctx* c, int K, const double* bnd, const double*
   if (o->rpsi_tr) o->rpsi_tr[0] = rpsi;
 
   for (int it = 0; it < K; ++it) {
+    z.it = it;
     /* step 2: xi1 (Eq. 13, 17, 4) */
     or_xi1_step(c, lam, g, bnd, xi1);
     /* step 3: xi2 with the convex surrogate (Eq. 18-19) */
     eval_vec(c->P, q, nv, xi1 + 1 * nv, tr.cc);
     eval_vec(c->P, q, nv, xi1 + 3 * nv, tr.ss);
-    heading_target(c, &tr);
+    if (model)
+      heading_target32(&z, xi1, &tr);
+    else
+      heading_target(c, &tr);
     or_xi2_step(c, lampsi, tr.theta, bnd, xi2);
     /* steps 4-5: xi3, xi4 closed forms (Eq. 20-22) on the new trajectory */
     eval_traj(c, xi1, xi2, &tr);
-    build_g(c, &tr, obs_xy, obs_ab, g);
+    if (model)
+      build_g32(&z, xi1, xi2, &tr, obs_xy, obs_ab, g);
+    else
+      build_g(c, &tr, obs_xy, obs_ab, g);
     /* step 6: multipliers (Eq. 23a-b, G3, G4) */
     resid_vec(c, xi1, g, res);
     mat_T_vec(c, res, ft);
@@ -629,7 +795,7 @@ int or_trace_instance(or_ctx* c, int K, const double* bnd, const double* obs_xy,
   o.theta_tr = theta_tr;
   o.r1_tr = r1_tr;
   o.rpsi_tr = rpsi_tr;
-  return run_instance(c, K, bnd, obs_xy, obs_ab, init, lambda_in, &o);
+  return run_instance(c, K, 0, bnd, obs_xy, obs_ab, init, lambda_in, &o);
 }
 
 int or_solve(or_ctx* c, int B, int K, long long index_base, const double* bnd,
@@ -653,7 +819,7 @@ int or_solve(or_ctx* c, int B, int K, long long index_base, const double* bnd,
     o.res = residual + 2 * (size_t)l;
     o.cost = cost + l;
     o.res_trace = res_trace ? res_trace + (size_t)l * K : NULL;
-    const int e = run_instance(c, K, bnd, obs_xy, obs_ab, init + (size_t)l * 3 * nv,
+    const int e = run_instance(c, K, index_base + l, bnd, obs_xy, obs_ab, init + (size_t)l * 3 * nv,
                                lambda_in ? lambda_in + (size_t)l * 5 * nv : NULL, &o);
     if (e != OR_OK) {
 #ifdef _OPENMP

@@ -50,6 +50,15 @@ typedef struct {
   int alpha_rule;          /* 0: alpha = atan2(yt, xt) (Eq. 21a); 1: atan2(a yt, b xt) (G8) */
   int lampsi_printed_sign; /* 0: gradient-consistent Eq. 23b (G4); 1: as printed */
   double res_tol;          /* feasibility threshold tau on r1 (G17)            */
+  /* fp32 rounding model (parity harness only):
+   * 0 = the oracle proper (fp64 throughout).  1 = the same iteration with every
+   * quantity that the product path holds in fp32 rounded to fp32 at the point
+   * where it is formed (round to nearest); with noise_seed != 0 those roundings
+   * are stochastic (up or down with probability given by the distance to the
+   * two fp32 neighbours, keyed by seed, instance, iteration, site, sample), so
+   * an ensemble of seeds measures how far fp32 rounding alone moves the result. */
+  int fp32_model;
+  unsigned long long noise_seed;
 } or_params;
 
 typedef struct or_ctx or_ctx;

@@ -34,7 +34,8 @@ class BmcParams(C.Structure):
 class BmcProblem(C.Structure):
     _fields_ = [("B", C.c_int64), ("index_base", C.c_int64), ("n_obs", C.c_int32),
                 ("iters", C.c_int32), ("bnd", C.c_double * 18), ("obs_xy", C.c_void_p),
-                ("obs_ab", C.c_void_p), ("init", C.c_void_p), ("lambda_in", C.c_void_p)]
+                ("obs_ab", C.c_void_p), ("init", C.c_void_p), ("lambda_in", C.c_void_p),
+                ("team", C.c_int32)]
 
 
 class BmcResult(C.Structure):
@@ -77,7 +78,10 @@ def load_library(path: str = LIBPATH):
         L.bmc_version.restype = C.c_int32
         L.bmc_last_launch_count.argtypes = [C.c_void_p]
         L.bmc_last_launch_count.restype = C.c_int32
-        L.bmc_pack_best.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.bmc_team_for.argtypes = [C.c_void_p, C.c_int64]
+        L.bmc_team_for.restype = C.c_int32
+        L.bmc_pack_best.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_void_p]
         L.bmc_pack_best.restype = C.c_int32
         L.bmc_select_best.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.bmc_select_best.restype = C.c_int32
@@ -132,10 +136,14 @@ class Solver:
 
     __del__ = close
 
-    def _problem(self, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base):
+    def team_for(self, B: int) -> int:
+        """bmc_team_for: the team size an automatic solve of B instances uses."""
+        return int(load_library().bmc_team_for(self._h, int(B)))
+
+    def _problem(self, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, team=0):
         bnd = np.ascontiguousarray(bnd, dtype=np.float64).reshape(18)
         return BmcProblem(B, index_base, n, iters, (C.c_double * 18).from_buffer_copy(bnd), _ptr(obs_xy),
-                          _ptr(obs_ab), _ptr(init), _ptr(lambda_in))
+                          _ptr(obs_ab), _ptr(init), _ptr(lambda_in), int(team))
 
     def _marshal(self, slot, arrays, scalars, bnd, build):
         """ctypes argument structs of the last call per entry point, reused while the
@@ -152,8 +160,9 @@ class Solver:
         return structs
 
     def solve(self, init, obs_xy, obs_ab, bnd, iters: int, lambda_in=None, trace: bool = False,
-              index_base: int = 0, out: Optional[dict] = None, stream=None) -> dict:
-        """Device solve on the current (or given) torch stream; returns device tensors."""
+              index_base: int = 0, out: Optional[dict] = None, stream=None, team: int = 0) -> dict:
+        """Device solve on the current (or given) torch stream; returns device tensors.
+        team: warps per instance (0 = automatic, see include/bmc.h)."""
         import torch
         dev = torch.device("cuda", self.device)
         B = int(init.shape[0])
@@ -163,12 +172,13 @@ class Solver:
             arrays = (init, obs_xy, obs_ab, lambda_in) + outs
             # torch storage can move under the same tensor object (resize_): key on addresses too
             addrs = tuple(t.data_ptr() if t is not None else 0 for t in arrays)
-            prob, res = self._marshal("dev", arrays, (B, n, iters, index_base) + addrs,
+            prob, res = self._marshal("dev", arrays, (B, n, iters, index_base, team) + addrs,
                                       bnd, lambda: self._dev_structs(dev, B, n, iters, bnd, obs_xy, obs_ab, init,
-                                                                     lambda_in, index_base, out))
+                                                                     lambda_in, index_base, out, team))
         else:
             out = self._dev_out(dev, B, iters, trace)
-            prob, res = self._dev_structs(dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out)
+            prob, res = self._dev_structs(dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out,
+                                          team)
         if stream is None:
             stream = torch.cuda.current_stream(dev)
         L = load_library()
@@ -190,13 +200,13 @@ class Solver:
             out["res_trace"] = torch.empty((B, iters), dtype=torch.float32, device=dev)
         return out
 
-    def _dev_structs(self, dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out):
+    def _dev_structs(self, dev, B, n, iters, bnd, obs_xy, obs_ab, init, lambda_in, index_base, out, team=0):
         import torch
         for name, t in (("init", init), ("obs_xy", obs_xy), ("obs_ab", obs_ab), ("lambda_in", lambda_in)):
             if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev):
                 raise ValueError(f"{name} must be a contiguous float32 tensor on {dev}")
         prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
-                             lambda_in, index_base)
+                             lambda_in, index_base, team)
         res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
                         _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
         return prob, res
@@ -219,7 +229,7 @@ class Solver:
 
     def solve_host(self, init: np.ndarray, obs_xy: np.ndarray, obs_ab: np.ndarray, bnd, iters: int,
                    lambda_in: Optional[np.ndarray] = None, trace: bool = False, index_base: int = 0,
-                   out: Optional[dict] = None) -> dict:
+                   out: Optional[dict] = None, team: int = 0) -> dict:
         """End-to-end solve from host arrays (pinned recommended); synchronous."""
         B = int(init.shape[0])
         n = int(obs_xy.shape[0]) if obs_xy is not None else 0
@@ -229,7 +239,7 @@ class Solver:
                 if a is not None and (a.dtype != np.float32 or not a.flags["C_CONTIGUOUS"]):
                     raise ValueError(f"{name} must be a C-contiguous float32 array")
             prob = self._problem(B, n, iters, bnd, obs_xy if n else None, obs_ab if n else None, init,
-                                 lambda_in, index_base)
+                                 lambda_in, index_base, team)
             res = BmcResult(_ptr(out["coeffs"]), _ptr(out.get("lambda_out")), _ptr(out["residual"]),
                             _ptr(out["cost"]), _ptr(out.get("res_trace")), _ptr(out["best"]))
             return prob, res
@@ -243,8 +253,8 @@ class Solver:
             prob, res = build()
         else:   # steady state: same buffers as the last call -> cached structs
             outs = tuple(out.get(k) for k in _OUT_KEYS)
-            prob, res = self._marshal("host", (init, obs_xy, obs_ab, lambda_in) + outs, (B, n, iters, index_base),
-                                      bnd, build)
+            prob, res = self._marshal("host", (init, obs_xy, obs_ab, lambda_in) + outs,
+                                      (B, n, iters, index_base, team), bnd, build)
         L = load_library()
         _check(L.bmc_solve_host(self._h, C.byref(prob), C.byref(res)))
         self.last_launches = L.bmc_last_launch_count(self._h)

@@ -62,13 +62,20 @@ struct HostBuf {  // context-owned device buffers for bmc_solve_host
 
 }  // namespace
 
+int32_t bmc::set_last_error(int32_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
 struct bmc_ctx {
   bmc_params p{};
   std::vector<double> r;
   int q = 0, QP = 0, NT = 0;
   std::map<int, Blob> blobs;   // by n_obs
-  unsigned long long* ws_key = nullptr;
+  unsigned long long* ws_key = nullptr;   // argmin workspace of bmc_solve
   unsigned int* ws_count = nullptr;
+  unsigned long long* ws_key_h = nullptr; // ... and of bmc_solve_host (its own stream)
+  unsigned int* ws_count_h = nullptr;
   cudaStream_t hstream = nullptr;
   HostBuf hb[10];
   int32_t last_launches = 0;
@@ -76,7 +83,7 @@ struct bmc_ctx {
 
 extern "C" {
 
-int32_t bmc_version(void) { return 101; }
+int32_t bmc_version(void) { return 102; }
 
 const char* bmc_last_error(void) { return g_err.c_str(); }
 
@@ -179,14 +186,18 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
   }
   DeviceGuard g(params->device);
   void* ws = nullptr;
-  e = cudaMalloc(&ws, 16);
+  e = cudaMalloc(&ws, 32);
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "cudaMalloc(workspace)");
   }
-  c->ws_key = reinterpret_cast<unsigned long long*>(ws);
-  c->ws_count = reinterpret_cast<unsigned int*>(reinterpret_cast<char*>(ws) + 8);
-  if ((e = cudaMemset(c->ws_key, 0xFF, 8)) != cudaSuccess || (e = cudaMemset(c->ws_count, 0, 8)) != cudaSuccess) {
+  char* wb = reinterpret_cast<char*>(ws);
+  c->ws_key = reinterpret_cast<unsigned long long*>(wb);
+  c->ws_count = reinterpret_cast<unsigned int*>(wb + 8);
+  c->ws_key_h = reinterpret_cast<unsigned long long*>(wb + 16);
+  c->ws_count_h = reinterpret_cast<unsigned int*>(wb + 24);
+  if ((e = cudaMemset(c->ws_key, 0xFF, 8)) != cudaSuccess || (e = cudaMemset(c->ws_count, 0, 8)) != cudaSuccess ||
+      (e = cudaMemset(c->ws_key_h, 0xFF, 8)) != cudaSuccess || (e = cudaMemset(c->ws_count_h, 0, 8)) != cudaSuccess) {
     bmc_destroy(c);
     return cuda_fail(e, "cudaMemset(workspace)");
   }
@@ -245,6 +256,8 @@ static int32_t validate_problem(const bmc_ctx* c, const bmc_problem* pr, const b
     return fail(BMC_EINVAL, "index_base + B must be in [1, 2^30]");
   if (pr->n_obs < 0 || pr->n_obs > N_MAX) return fail(BMC_EINVAL, "n_obs must be in [0, 160]");
   if (pr->iters < 0) return fail(BMC_EINVAL, "iters must be >= 0");
+  if (pr->team != 0 && pr->team != 1 && pr->team != 2 && pr->team != 4)
+    return fail(BMC_EINVAL, "team must be 0, 1, 2 or 4");
   if (pr->n_obs > 0 && (!pr->obs_xy || !pr->obs_ab)) return fail(BMC_EINVAL, "obs_xy / obs_ab is NULL");
   if (!pr->init) return fail(BMC_EINVAL, "init is NULL");
   if (!rs->coeffs || !rs->residual || !rs->cost || !rs->best)
@@ -260,15 +273,13 @@ static int32_t validate_problem(const bmc_ctx* c, const bmc_problem* pr, const b
   return BMC_OK;
 }
 
-static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, cudaStream_t s) {
-  Blob* blob = nullptr;
-  int32_t rc = get_blob(c, pr->n_obs, &blob);
-  if (rc != BMC_OK) return rc;
-  // launch shape: `team` warps per instance, `ipc` instances per CTA.  One
-  // warp per instance by default; BMC_TEAM / BMC_IPC override (experiments).
-  // Occupancy model: <= 16 warps per SM (<= 128 registers per thread); the
-  // batch is spread so that every SM holds ceil(B / 148) instances, and
-  // small batches spend the spare warps on teams (one 32-sample round each).
+// Launch shape: `team` warps per instance, `ipc` instances per CTA.
+// Occupancy model: <= 16 warps per SM (<= 128 registers per thread); the
+// batch is spread so that every SM holds ceil(B / 148) instances, and small
+// batches spend the spare warps on teams (one 32-sample round each).
+// team_req != 0 fixes the team; BMC_TEAM / BMC_IPC / BMC_WMAX / BMC_WCTA
+// override the automatic choice (experiments).
+static void launch_shape(const bmc_ctx* c, int64_t B, int32_t team_req, int* ipc_out, int* team_out) {
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->p.device);
   const int rounds = (c->q + 31) / 32;
@@ -278,16 +289,39 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   // needed at wmax, then the fewest instances per CTA that still fit in them
   // (B = 4096: 2 waves of 14 instead of 1.73 waves of 16 -- every wave costs
   // the same time, and fewer warps per SM run each wave faster)
-  const int64_t waves = std::max<int64_t>(1, (pr->B + (int64_t)dev_sms * wmax - 1) / ((int64_t)dev_sms * wmax));
-  int ipc = (int)std::min<int64_t>(wmax, (pr->B + dev_sms * waves - 1) / (dev_sms * waves));
+  const int64_t waves = std::max<int64_t>(1, (B + (int64_t)dev_sms * wmax - 1) / ((int64_t)dev_sms * wmax));
+  int ipc = (int)std::min<int64_t>(wmax, (B + dev_sms * waves - 1) / (dev_sms * waves));
   int team = std::max(1, std::min(rounds, wmax / std::max(1, ipc)));
-  if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
-  if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
-  if (team < 1 || team > 4) team = 1;
-  if (team == 3) team = (ipc * 4 <= wmax) ? 4 : 2;   // kernels exist for teams of 1, 2, 4
+  if (team_req == 0) {
+    if (const char* s = std::getenv("BMC_TEAM")) team = std::atoi(s);
+    if (const char* s = std::getenv("BMC_IPC")) ipc = std::atoi(s);
+    if (team < 1 || team > 4) team = 1;
+    if (team == 3) team = (ipc * 4 <= wmax) ? 4 : 2;   // kernels exist for teams of 1, 2, 4
+  } else {
+    team = team_req;
+  }
   int wcta = 16;   // warps per CTA (__launch_bounds__(512)); BMC_WCTA: register-capped experiment builds
   if (const char* s = std::getenv("BMC_WCTA")) wcta = std::max(1, std::min(32, std::atoi(s)));
   if (ipc < 1 || ipc * team > wcta) ipc = std::max(1, wcta / team);
+  *ipc_out = ipc;
+  *team_out = team;
+}
+
+int32_t bmc_team_for(const bmc_ctx* c, int64_t B) {
+  if (!c || B < 1) return 0;
+  DeviceGuard g(c->p.device);
+  int ipc = 1, team = 1;
+  launch_shape(c, B, 0, &ipc, &team);
+  return team;
+}
+
+static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, cudaStream_t s,
+                          unsigned long long* ws_key, unsigned int* ws_count) {
+  Blob* blob = nullptr;
+  int32_t rc = get_blob(c, pr->n_obs, &blob);
+  if (rc != BMC_OK) return rc;
+  int ipc = 1, team = 1;
+  launch_shape(c, pr->B, pr->team, &ipc, &team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024) --ipc;
   if (kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024)
     return fail(BMC_EINVAL, "n_obs * q too large for shared memory");
@@ -305,8 +339,8 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   a.cost = rs->cost;
   a.res_trace = (pr->iters > 0) ? rs->res_trace : nullptr;
   a.best = reinterpret_cast<long long*>(rs->best);
-  a.ws_key = c->ws_key;
-  a.ws_count = c->ws_count;
+  a.ws_key = ws_key;
+  a.ws_count = ws_count;
   a.B = pr->B;
   a.index_base = pr->index_base;
   a.q = c->q;
@@ -446,7 +480,7 @@ int32_t bmc_solve(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, bmc_s
   if (rc != BMC_OK) return rc;
   DeviceGuard g(c->p.device);
   c->last_launches = 0;
-  rc = solve_impl(c, pr, rs, reinterpret_cast<cudaStream_t>(stream));
+  rc = solve_impl(c, pr, rs, reinterpret_cast<cudaStream_t>(stream), c->ws_key, c->ws_count);
   if (rc == BMC_OK) g_err.clear();
   return rc;
 }
@@ -520,7 +554,7 @@ int32_t bmc_solve_host(bmc_ctx* c, const bmc_problem* ph, const bmc_result* rh) 
   }
   if (!m_init) H2D(d[2], ph->init, sz[2]);
   if (ph->lambda_in && !m_lam) H2D(d[3], ph->lambda_in, sz[3]);
-  rc = solve_impl(c, &pd, &rd, s);
+  rc = solve_impl(c, &pd, &rd, s, c->ws_key_h, c->ws_count_h);
   if (rc != BMC_OK) return rc;
   if (!m_co) D2H(rh->coeffs, d[4], sz[4]);
   if (rh->lambda_out && !m_lo) D2H(rh->lambda_out, d[5], sz[5]);

@@ -20,14 +20,21 @@ namespace {
 constexpr int REC = 32;   // int64 words per record: key, 55 floats packed, pad
 
 __global__ void pack_best_kernel(const long long* __restrict__ best, const float* __restrict__ coeffs,
+                                 const float* __restrict__ residual, const float* __restrict__ cost,
                                  long long index_base, long long* __restrict__ record) {
   const int lane = threadIdx.x;
   const long long key = best[1];
   const long long local = best[0] - index_base;   // instance within this shard
+  const bool empty = key == -1ll;                 // empty shard: key ~0, no coefficients
   float* rf = reinterpret_cast<float*>(record + 1);
   if (lane == 0) record[0] = key;
-  for (int k = lane; k < 5 * NV; k += 32) rf[k] = coeffs[local * 5 * NV + k];
-  for (int k = 5 * NV + lane; k < 2 * (REC - 1); k += 32) rf[k] = 0.f;
+  for (int k = lane; k < 5 * NV; k += 32) rf[k] = empty ? 0.f : coeffs[local * 5 * NV + k];
+  for (int k = 5 * NV + lane; k < 2 * (REC - 1); k += 32) {
+    float v = 0.f;   // floats 55, 56, 57: r1, r_psi, J of the instance
+    if (!empty && residual && k < 5 * NV + 2) v = residual[local * 2 + (k - 5 * NV)];
+    if (!empty && cost && k == 5 * NV + 2) v = cost[local];
+    rf[k] = v;
+  }
 }
 
 __global__ void select_best_kernel(const long long* __restrict__ records, int nranks,
@@ -56,27 +63,35 @@ __global__ void select_best_kernel(const long long* __restrict__ records, int nr
 }  // namespace bmc
 
 namespace {
-thread_local std::string g_xerr;
+int32_t launch_status(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    bmc::set_last_error(BMC_OK, "");
+    return BMC_OK;
+  }
+  return bmc::set_last_error(BMC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+}  // namespace
 
 extern "C" {
 
-int32_t bmc_pack_best(const int64_t* best, const float* coeffs, int64_t index_base, int64_t* record,
-                      bmc_stream_t stream) {
-  if (!best || !coeffs || !record) return BMC_EINVAL;
+int32_t bmc_pack_best(const int64_t* best, const float* coeffs, const float* residual, const float* cost,
+                      int64_t index_base, int64_t* record, bmc_stream_t stream) {
+  if (!best || !coeffs || !record) return bmc::set_last_error(BMC_EINVAL, "bmc_pack_best: NULL pointer");
   bmc::pack_best_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const long long*>(best), coeffs, (long long)index_base,
+      reinterpret_cast<const long long*>(best), coeffs, residual, cost, (long long)index_base,
       reinterpret_cast<long long*>(record));
-  return cudaGetLastError() == cudaSuccess ? BMC_OK : BMC_ECUDA;
+  return launch_status("pack_best_kernel launch");
 }
 
 int32_t bmc_select_best(const int64_t* records, int32_t nranks, int64_t* best_out, float* coeffs_out,
                         bmc_stream_t stream) {
-  if (!records || nranks < 1 || !best_out || !coeffs_out) return BMC_EINVAL;
+  if (!records || !best_out || !coeffs_out) return bmc::set_last_error(BMC_EINVAL, "bmc_select_best: NULL pointer");
+  if (nranks < 1) return bmc::set_last_error(BMC_EINVAL, "bmc_select_best: nranks < 1");
   bmc::select_best_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const long long*>(records), nranks, reinterpret_cast<long long*>(best_out),
       coeffs_out);
-  return cudaGetLastError() == cudaSuccess ? BMC_OK : BMC_ECUDA;
+  return launch_status("select_best_kernel launch");
 }
 
 }  // extern "C"

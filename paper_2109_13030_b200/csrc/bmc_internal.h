@@ -115,6 +115,9 @@ struct HostConsts {
   ~HostConsts() { delete[] pt; delete[] pt64; }
 };
 
+// bmc_api.cpp: set the calling thread's bmc_last_error() message; returns code.
+int32_t set_last_error(int32_t code, const std::string& msg);
+
 // setup.cpp: fp64 constants for obstacle count n; 0 or 2 (singular) with *err.
 int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err);
 

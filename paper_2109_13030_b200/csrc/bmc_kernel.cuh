@@ -34,6 +34,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <atomic>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -146,12 +148,12 @@ __host__ __device__ inline int pad_obstacles(int n) { return (n + JB - 1) / JB *
 __host__ __device__ inline int clr_stride(int n) { return pad_obstacles(n) + JB; }
 
 // Layout after the constant blob: obstacles [npad + 1][QP] (row npad: the far
-// dummy), abi [npad + 1], u = K12 b, WarpSmem[ipc], clearance stamps
+// dummy), abi [npad + 1], ell [npad + 1], u = K12 b, WarpSmem[ipc], clearance stamps
 // [ipc][4][nclr], active lists [ipc * T][nclr], D2 partials [ipc * T][HP_SLOTS],
 // the mbarrier of the blob copy.
 __host__ __device__ inline size_t smem_bytes(int n, int ipc, int T) {
   const int np = pad_obstacles(n) + 1;
-  return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + (size_t)np * sizeof(float4) +
+  return BlobLayout::bytes(QP) + (size_t)np * QP * sizeof(float2) + 2 * (size_t)np * sizeof(float4) +
          U_DOUBLES * sizeof(double) + (size_t)ipc * ws_bytes(T) +
          (size_t)ipc * (T_MAX + T) * clr_stride(n) * sizeof(float) +
          (T > 1 ? (size_t)ipc * T * HP_SLOTS * sizeof(double) : 0) +
@@ -392,8 +394,10 @@ struct Proj {
   const double* Pt64;    // the same basis in fp64 (contractions)
   const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
   const float4* abi;     // smem (a, b, a b, kind) per obstacle
+  const float4* ell;     // smem (1/a, 1/b, max(a, b), 0) per obstacle (culled ellipses, NEXT-4)
   int q, n, rounds;
-  bool all_circ;
+  bool all_circ;         // every obstacle a circle (a = b): culled closed form
+  bool all_cull;         // every obstacle a circle or a scaled-rule ellipse (G8): culled, ELL form
   float nR1, nR2p1, v_max, a_max;
   float rabs;            // max_i |r_i| (culling clock)
   float* clr;            // smem clearance stamps of the instance, [4 rounds][nclr]
@@ -428,9 +432,14 @@ struct Proj {
 // NB obstacles of the active list (one basic block: their loads and MUFU
 // latencies overlap), then the warp reductions of their stamps.  Returns true
 // in some lane if a circle centre sits exactly on an obstacle centre (G18).
-template <int M, int NB>
+// ELL (NEXT-4, scenes with scaled-rule ellipses, G8): the closed form of the
+// scaled rule, delta = (x~, y~) max(1 / |(x~ / a, y~ / b)| - 1, 0), exactly zero
+// outside the ellipse, with the stamp taken against the bounding circle of
+// radius max(a, b) (ell[j] = (1/a, 1/b, max(a, b), 0); circles: a = b).
+template <int M, int NB, bool ELL>
 __device__ __forceinline__ bool coll_block(const bool RES, const float2* __restrict__ ob,
-                                           const float4* __restrict__ abi, const int* __restrict__ list, int jb,
+                                           const float4* __restrict__ abi, const float4* __restrict__ ell,
+                                           const int* __restrict__ list, int jb,
                                            float* __restrict__ clr, float A, int lane, const float2 (&XY)[M],
                                            const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
                                            float& rc) {
@@ -440,12 +449,20 @@ __device__ __forceinline__ bool coll_block(const bool RES, const float2* __restr
     const int j = list[jb + jj];
     const float2 o = ob[j * QP];
     const float a = abi[j].x;
+    float2 inv = make_float2(0.f, 0.f);
+    if (ELL) inv = *reinterpret_cast<const float2*>(&ell[j]);
     float r2min = INFINITY;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const float2 tt = sub2(XY[i], o);   // (x~, y~)
       const float r2 = fmaf(tt.y, tt.y, tt.x * tt.x);
-      const float sc = fmaxf(fmaf(a, rsqrt_ftz(r2), -1.f), 0.f);
+      float sc;
+      if (ELL) {
+        const float2 u = mul2(tt, inv);   // (x~ / a, y~ / b)
+        sc = fmaxf(rsqrt_ftz(fmaf(u.y, u.y, u.x * u.x)) - 1.f, 0.f);
+      } else {
+        sc = fmaxf(fmaf(a, rsqrt_ftz(r2), -1.f), 0.f);
+      }
       const float2 dd = mul2(bc2(sc), tt);
       D[i] = add2(D[i], dd);
       if (RES) rc = fmaf(dd.x, dd.x - 2.f * rec[i], fmaf(dd.y, dd.y - 2.f * res_s[i], rc));
@@ -462,7 +479,7 @@ __device__ __forceinline__ bool coll_block(const bool RES, const float2* __restr
   }
   if (lane < NB) {
     const int j = list[jb + lane];
-    clr[j] = sqrt_approx(__uint_as_float(qm)) - abi[j].x * 1.00001f + A;
+    clr[j] = sqrt_approx(__uint_as_float(qm)) - (ELL ? ell[j].z : abi[j].x) * 1.00001f + A;
   }
   return qm == 0u;
 }
@@ -470,9 +487,10 @@ __device__ __forceinline__ bool coll_block(const bool RES, const float2* __restr
 // The active list in blocks of JB obstacles, then a block of 2 and one of 1
 // for the remainder: most rounds have one or two active obstacles, and padding
 // them to a block of 4 with far dummies cost 1-3 % (C3, C4).
-template <int M>
+template <int M, bool ELL>
 __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __restrict__ ob,
-                                              const float4* __restrict__ abi, const int* __restrict__ list, int na,
+                                              const float4* __restrict__ abi, const float4* __restrict__ ell,
+                                              const int* __restrict__ list, int na,
                                               float* __restrict__ clr, float A, int lane, const float2 (&XY)[M],
                                               const float (&rec)[M], const float (&res_s)[M], float2 (&D)[M],
                                               float& rc) {
@@ -480,12 +498,12 @@ __device__ __forceinline__ unsigned coll_circ(const bool RES, const float2* __re
   int jb = 0;
 #pragma unroll 1
   for (; jb + JB <= na; jb += JB)
-    zero |= coll_block<M, JB>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
+    zero |= coll_block<M, JB, ELL>(RES, ob, abi, ell, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
   if (jb + 2 <= na) {
-    zero |= coll_block<M, 2>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
+    zero |= coll_block<M, 2, ELL>(RES, ob, abi, ell, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
     jb += 2;
   }
-  if (jb < na) zero |= coll_block<M, 1>(RES, ob, abi, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
+  if (jb < na) zero |= coll_block<M, 1, ELL>(RES, ob, abi, ell, list, jb, clr, A, lane, XY, rec, res_s, D, rc);
   return __any_sync(FULL, zero) ? 1u : 0u;
 }
 
@@ -573,9 +591,11 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
   float2 ccs[NV];   // (c_c, c_s) per Bernstein index
 #pragma unroll
   for (int k = 0; k < NV; ++k) ccs[k] = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
+#ifndef BMC_THETA_MMA
   double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+#endif
   const int nr = (q + 31) >> 5;
 #pragma unroll 2
   for (int uu = 0; uu < QP / 32; ++uu) {   // two rounds in flight: independent atan2 chains
@@ -591,15 +611,56 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     const float tht = atan2_fast(cs.y, cs.x);   // atan2(0, 0) = 0 (G18)
     ws->cs[t] = cs;
     ws->th[t] = tht;
+#ifndef BMC_THETA_MMA
     const double thd = f2d(tht);
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
+#endif
   }
+#ifndef BMC_THETA_MMA
   // 11 entries as 8 + 4 transpose-reduce slots
   const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
   const double v4 = tr_reduce<4>(acc + 8, lane);    // entry 8 + (lane >> 3)
   if (!(lane & 3)) ws->part_th[w][lane >> 2] = v8;
   if (!(lane & 7) && 8 + (lane >> 3) < NV) ws->part_th[w][8 + (lane >> 3)] = v4;
+#else
+  // P^T theta on the FP64 tensor cores: G = P^T [theta .. theta] (every column the
+  // same; column 0 is kept), k = 4 samples per m8n8k4 step, the basis as the A
+  // fragment (as in D2), theta of the warp's rounds as the B fragment
+  __syncwarp();   // the rounds' theta are in shared memory
+  const int aoff0 = (lane >> 2) * QP64 + (lane & 3), aoff1 = min(8 + (lane >> 2), NV - 1) * QP64 + (lane & 3);
+  const float* __restrict__ thc = &ws->th[lane & 3];
+  double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
+#pragma unroll 1
+  for (int u = T - 1 - w; u < nr; u += T) {
+    const int t0 = 32 * u;
+    if (t0 + 32 <= q) {
+#pragma unroll
+      for (int st = 0; st < 8; ++st) {
+        const double b = f2d(thc[t0 + 4 * st]);
+        if (st & 1) {
+          mma_f64_884(e0, Pt64[aoff0 + t0 + 4 * st], b);
+          mma_f64_884(e1, Pt64[aoff1 + t0 + 4 * st], b);
+        } else {
+          mma_f64_884(g0, Pt64[aoff0 + t0 + 4 * st], b);
+          mma_f64_884(g1, Pt64[aoff1 + t0 + 4 * st], b);
+        }
+      }
+    } else {
+      const int ns = (q - t0 + 3) >> 2;
+#pragma unroll 1
+      for (int st = 0; st < ns; ++st) {
+        const double b = f2d(thc[t0 + 4 * st]);
+        mma_f64_884(g0, Pt64[aoff0 + t0 + 4 * st], b);
+        mma_f64_884(g1, Pt64[aoff1 + t0 + 4 * st], b);
+      }
+    }
+  }
+  if (!(lane & 3)) {
+    ws->part_th[w][lane >> 2] = g0[0] + e0[0];
+    if (8 + (lane >> 2) < NV) ws->part_th[w][8 + (lane >> 2)] = g1[0] + e1[0];
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- phase D
@@ -716,12 +777,12 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     float rc = 0.f;
     const float2* ob = pa.obs + t;
     BMC_SUB(pc, 12);   // evaluation, velocity / acceleration, heading
-    // circular obstacles: culled closed forms (coll_circ); ellipses: the plain
-    // loop.  x~ = y~ = 0 exactly (G18, rare: detected by the stamp reductions
-    // for circles, by a non-finite sum for ellipses) reruns the round with the
-    // guarded plain loop; one call site keeps the hot loop small in the
-    // instruction cache.
-    bool general = !pa.all_circ;
+    // circular obstacles and scaled-rule ellipses: culled closed forms
+    // (coll_circ); literal-rule ellipses: the plain loop.  x~ = y~ = 0 exactly
+    // (G18, rare: detected by the stamp reductions when culled, by a non-finite
+    // sum in the plain loop) reruns the round with the guarded plain loop; one
+    // call site keeps the hot loop small in the instruction cache.
+    bool general = !pa.all_cull;
     bool rerun = false;   // warp-uniform: x~ = y~ = 0 exactly somewhere -> guarded pass (G18)
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
@@ -742,7 +803,10 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #endif
       BMC_SUB(pc, 13);   // culling clock and active list
       // the exact zero shows up in the stamp reductions (a round minimum r2 of 0)
-      rerun = coll_circ<M>(RES, ob, pa.abi, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
+      if (pa.all_circ)
+        rerun = coll_circ<M, false>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
+      else
+        rerun = coll_circ<M, true>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
     }
     bool guard = false;
 #pragma unroll 1
@@ -862,7 +926,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   float2* obs = reinterpret_cast<float2*>(smem + BlobLayout::bytes(QP));
   const int npad = pad_obstacles(n), nclr = clr_stride(n);
   float4* abi = reinterpret_cast<float4*>(obs + (size_t)(npad + 1) * QP);
-  double* ub = reinterpret_cast<double*>(abi + npad + 1);
+  float4* ell = abi + npad + 1;
+  double* ub = reinterpret_cast<double*>(ell + npad + 1);
   using WarpSmem = WarpSmemT<TT>;
   WarpSmem* wsbase = reinterpret_cast<WarpSmem*>(ub + U_DOUBLES);
   constexpr int T = TT;                              // warps per instance (compile time: folds the
@@ -920,15 +985,20 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
     obs[idx] = v;
   }
-  int circ = 1;
-  for (int j = n + tid; j <= npad; j += blockDim.x) abi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  int circ = 1, cull = 1;
+  for (int j = n + tid; j <= npad; j += blockDim.x) {   // far dummies: zero offset under either form
+    abi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ell[j] = make_float4(1.f, 1.f, 0.f, 0.f);
+  }
   for (int i = tid; i < ipc * T_MAX * nclr; i += blockDim.x) clr_base[i] = -1.0e30f;   // never tested
   for (int j = tid; j < n; j += blockDim.x) {
     const float aa = __ldg(a.obs_ab + 2 * j), bb = __ldg(a.obs_ab + 2 * j + 1);
     const float kind = (aa == bb) ? 0.f : (a.alpha_rule == 0 ? 1.f : 2.f);
     // z: a b (numerator of the scaled rule, coll_general)
     abi[j] = make_float4(aa, bb, aa * bb, kind);
+    ell[j] = make_float4(1.f / aa, 1.f / bb, fmaxf(aa, bb), 0.f);
     circ &= (aa == bb);
+    cull &= (kind != 1.f);   // the literal rule has no zero offset outside the ellipse (G8)
   }
   for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
     (&wsbase[i / ((NV + 1) * 8)].cfi[0][0])[i % ((NV + 1) * 8)] = 0.f;
@@ -939,6 +1009,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     (&wsbase[i / (3 * QP + 2 * T_MAX)].pxy[0].x)[i % (3 * QP + 2 * T_MAX)] = 0.f;
   BMC_STAMP(4);   // staging loops issued (thread 0)
   const bool all_circ = __syncthreads_and(circ);
+  const bool all_cull = __syncthreads_and(cull);
   BMC_STAMP(5);   // staging done
   mbar_wait(mbar, 0);
   BMC_STAMP(6);   // blob landed
@@ -970,6 +1041,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   pa.n = n;
   pa.rounds = (q + 31) / 32;
   pa.all_circ = all_circ;
+  pa.all_cull = all_cull;
+  pa.ell = ell;
   pa.nR1 = a.nR1;
   pa.nR2p1 = a.nR2p1;
   pa.v_max = a.v_max;
@@ -1258,12 +1331,18 @@ size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 // Launch of one (M, team size) kernel variant.
 template <int M, int TT>
 cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  // the shared-memory opt-in is per device: one bit per device ordinal (set on
+  // the current device, which bmc_solve made params.device); racing threads
+  // both set the attribute, which is idempotent
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (dev >= 64 || !(attr_done.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done.fetch_or(bit, std::memory_order_release);
 #ifdef BMC_PROFILE
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT>) == cudaSuccess)

@@ -27,6 +27,7 @@ control loop itself is host logic around the hot path.
 """
 from __future__ import annotations
 
+import ctypes as C
 import functools
 
 from dataclasses import dataclass, field
@@ -36,6 +37,8 @@ from typing import Callable, Optional
 import numpy as np
 
 from synth import Config, make_init, tracks_at
+
+from .distributed import RECORD_WORDS, pack_record
 
 
 @dataclass(frozen=True)
@@ -185,7 +188,10 @@ class GpuBackend:
             self.out = [dict(coeffs=mk(B, 5, 11), lambda_out=mk(B, 5, 11), residual=mk(B, 2), cost=mk(B),
                              best=torch.empty(2, dtype=torch.int64, device=self.dev)) for _ in range(2)]
             self.flip = 0
-            self.rb = torch.empty(58, dtype=torch.float32).pin_memory()   # read-back: coeffs, residual, cost
+            # read-back of the best instance: bmc_pack_best gathers {key, 55 coefficients,
+            # r1, r_psi, J} on the device into one 256-byte record, copied once per tick
+            self.rec = torch.empty(RECORD_WORDS, dtype=torch.int64, device=self.dev)
+            self.rb = torch.empty(RECORD_WORDS, dtype=torch.int64).pin_memory()
         o = self.out[self.flip]          # double-buffered: lambda_in of this tick is the other buffer
         self.flip ^= 1
         stream = torch.cuda.current_stream(self.dev)
@@ -193,16 +199,13 @@ class GpuBackend:
         self.solver.solve(init_d, obs_d if obs_xy.shape[0] else None, ab_d if obs_xy.shape[0] else None, bnd, K,
                           lambda_in=lam, out=o)
         self.ev[1].record(stream)
-        # one read-back per tick: the best instance's 55 coefficients, residuals and cost
-        # gathered on the device, then a single D2H into pinned memory
-        i = o["best"][:1]
-        self.rb.copy_(torch.cat((o["coeffs"].view(B, 55).index_select(0, i).view(55),
-                                 o["residual"].index_select(0, i).view(2), o["cost"].index_select(0, i))),
-                      non_blocking=True)
-        best_t = o["best"][0].to("cpu", non_blocking=True)
+        # one read-back per tick: the best instance's record, gathered by the library
+        pack_record(o["best"], o["coeffs"], 0, self.rec, C.c_void_p(stream.cuda_stream), o["residual"], o["cost"])
+        self.rb.copy_(self.rec, non_blocking=True)
         stream.synchronize()
-        rb = self.rb.numpy()
-        res = dict(lambda_out=o["lambda_out"], best=int(best_t), best_coeffs=rb[:55].copy(),
+        key = int(self.rb[0])
+        rb = self.rb.numpy()[1:].view(np.float32)
+        res = dict(lambda_out=o["lambda_out"], best=key & ((1 << 30) - 1), best_coeffs=rb[:55].copy(),
                    best_residual=rb[55:57].copy(), best_cost=float(rb[57]))
         res["solve_ms"] = self.ev[0].elapsed_time(self.ev[1])
         return res

@@ -1,45 +1,58 @@
 """GPU <-> oracle comparison used by the -m gpu tests and smoke().
 
-Tolerances (BASELINE.json north_star):
-  * trajectory: max over t and the x, y channels of |P (c_gpu - c_oracle)| <= 1e-3 m,
+The bar (BASELINE.json north_star), per instance:
+  * trajectory x, y: max over t of |P (c_gpu - c_oracle)| <= TRAJ_TOL = 1e-3 m,
     with P the fp64 basis (scipy BPoly, independent of both sides);
+  * heading psi and the copies c, s (the rest of the trajectory):
+    <= ANGLE_TOL = 1e-3 rad (dimensionless for c, s) -- reading P1 of DESIGN.md:
+    1e-3 rad moves a circle centre (|r_i| <= 0.75 m) by < 1e-3 m;
   * cost J: |dJ| <= 1e-4 |J| + 1e-8 q;
   * residuals r1, r_psi: |dr| <= 1e-4 |r| + RES_FLOOR, RES_FLOOR = 2e-5: the GPU
     evaluates the per-row residuals in fp32, so each row carries ~1e-7 absolute
     rounding and ||.||_2 over ~1e4 rows an absolute floor of ~1e-5;
+  * multipliers lambda_out: max |d lambda| <= 1e-4 max|lambda| + LAM_FLOOR (the
+    north star's relative 1e-4, norm-wise: the entries differ by orders of
+    magnitude); LAM_FLOOR = rho K sqrt(q) 3e-7 is K multiplier steps of a
+    contraction over q samples of fp32 residuals (~3e-7 absolute each);
   * best index identical, unless the scene is ambiguous (a residual within 1e-3
     relative of tau, or the oracle's best and runner-up keys within 1e-3
-    relative): then the GPU's pick must be within 1e-4 of the oracle's best value.
+    relative): then the oracle's value at the GPU's pick must be within 1e-4 of
+    the oracle's best value.
 
-Ill-conditioned instances: the AM iteration is a
-non-smooth, non-convex map; on some instances it amplifies perturbations by
->1e3 over 100 iterations, so a one-ulp (fp32) change of the input moves the
-fp64 oracle's own answer by more than the tolerance.  For an instance that
-misses the bar, the oracle is re-run on `N_PERT` copies of its input with the
-interior control points perturbed by `PERT_REL` (relative, the fp32 input
-rounding scale) and the obstacle positions by `PERT_OBS` (absolute, the fp32
-rounding of positions in the kernel's deviation frame: |x - x_ref| <= 30 m has
-an ulp of 2e-6 m); the instance passes only if the GPU deviation is within
-`KAPPA` times that spread for every quantity that misses the bar.  The kernel
-rounds at that scale in every iteration, not once at the input, hence the
-factor; a well-conditioned instance (spread ~1e-7) still gets no slack.  At
-full C3 size about 0.5 % of the instances need this.
-Every such acceptance is reported.
+fp32 rounding model: the AM map is non-smooth and
+non-convex; on some instances it amplifies perturbations by >1e3 over 100
+iterations, so fp32 rounding ALONE moves the answer by more than the bar and no
+fp32 implementation can meet it there.  For an instance that misses the bar, the
+oracle is re-run N_MODEL times with its fp32 rounding model (oracle.h
+`fp32_model`: every quantity the product path holds in fp32 rounded where it is
+formed, stochastically, one seed per run); the instance passes only if, for
+every quantity that misses the bar, the GPU deviation is within KAPPA times the
+largest deviation of those runs from the fp64 oracle.  KAPPA is calibrated on
+the oracle alone (tools/calibrate_kappa.py): further model runs standing in
+for "another fp32 implementation" stay within KAPPA x the N_MODEL-run spread on
+every calibration instance.  A well-conditioned instance (model spread ~1e-6)
+gets no slack.  Every such acceptance is reported.
 """
 from __future__ import annotations
+
+import dataclasses
 
 import numpy as np
 
 from tests.helpers import bpoly_basis
 
 TRAJ_TOL = 1e-3
+ANGLE_TOL = 1e-3
 COST_RTOL = 1e-4
 RES_RTOL = 1e-4
 RES_FLOOR = 2e-5
-PERT_REL = 1e-7
-PERT_OBS = 1e-6
-N_PERT = 3
-KAPPA = 10.0
+LAM_RTOL = 1e-4
+LAM_UNIT = 3e-7          # absolute fp32 rounding of one residual sample (LAM_FLOOR)
+N_MODEL = 4              # fp32-model runs per failing instance
+MODEL_SEED0 = 1          # their seeds: MODEL_SEED0 .. MODEL_SEED0 + N_MODEL - 1
+KAPPA = 3.0              # tools/calibrate_kappa.py (profiles/kappa_calibration.json)
+
+QUANTITIES = ("traj", "psi", "copy", "cost", "r1", "rpsi", "lam")
 
 
 def key_value(r1, J, tau):
@@ -48,87 +61,113 @@ def key_value(r1, J, tau):
     return feas, v
 
 
-def _deviations(P, cg, cr, Jg, Jr, rg, rr):
-    cg = np.asarray(cg, dtype=np.float64)
-    cr = np.asarray(cr, dtype=np.float64)
-    dtraj = np.zeros(cg.shape[0])
-    for blk in (0, 2):
-        dtraj = np.maximum(dtraj, np.max(np.abs((cg[:, blk] - cr[:, blk]) @ P.T), axis=1))
-    dJ = np.abs(np.asarray(Jg, np.float64) - np.asarray(Jr, np.float64))
-    dr = np.abs(np.asarray(rg, np.float64) - np.asarray(rr, np.float64))
-    return dtraj, dJ, dr
+def deviations(P, g: dict, r: dict) -> dict:
+    """Per-instance deviation of each quantity between two result sets."""
+    cg = np.asarray(g["coeffs"], np.float64)
+    cr = np.asarray(r["coeffs"], np.float64)
+    ev = lambda blk: np.max(np.abs((cg[:, blk] - cr[:, blk]) @ P.T), axis=1)
+    rg = np.asarray(g["residual"], np.float64)
+    rr = np.asarray(r["residual"], np.float64)
+    d = dict(traj=np.maximum(ev(0), ev(2)), psi=ev(4), copy=np.maximum(ev(1), ev(3)),
+             cost=np.abs(np.asarray(g["cost"], np.float64) - np.asarray(r["cost"], np.float64)),
+             r1=np.abs(rg[:, 0] - rr[:, 0]), rpsi=np.abs(rg[:, 1] - rr[:, 1]))
+    if "lambda_out" in g and "lambda_out" in r:
+        lg = np.asarray(g["lambda_out"], np.float64).reshape(len(cg), -1)
+        lr = np.asarray(r["lambda_out"], np.float64).reshape(len(cg), -1)
+        d["lam"] = np.max(np.abs(lg - lr), axis=1)
+    return d
 
 
-def _fails(cfg, dtraj, dJ, dr, Jr, rr, scale=None):
-    """Per-instance bar; `scale` = (traj, cost, res) allowances replacing the tolerances."""
-    tt = TRAJ_TOL if scale is None else np.maximum(TRAJ_TOL, scale[0])
-    tJ = COST_RTOL * np.abs(Jr) + 1e-8 * cfg.q
-    tr = RES_RTOL * np.abs(rr) + RES_FLOOR
-    if scale is not None:
-        tJ = np.maximum(tJ, scale[1])
-        tr = np.maximum(tr, scale[2][:, None] if np.ndim(scale[2]) == 1 else scale[2])
-    return (dtraj > tt) | (dJ > tJ) | np.any(dr > tr, axis=1)
+def bars(cfg, r: dict, iters: int) -> dict:
+    """Per-instance tolerance of each quantity (module docstring)."""
+    J = np.abs(np.asarray(r["cost"], np.float64))
+    rr = np.abs(np.asarray(r["residual"], np.float64))
+    n = len(J)
+    b = dict(traj=np.full(n, TRAJ_TOL), psi=np.full(n, ANGLE_TOL), copy=np.full(n, ANGLE_TOL),
+             cost=COST_RTOL * J + 1e-8 * cfg.q, r1=RES_RTOL * rr[:, 0] + RES_FLOOR,
+             rpsi=RES_RTOL * rr[:, 1] + RES_FLOOR)
+    if "lambda_out" in r:
+        lam = np.abs(np.asarray(r["lambda_out"], np.float64)).reshape(n, -1).max(axis=1)
+        b["lam"] = LAM_RTOL * lam + cfg.rho * max(iters, 1) * np.sqrt(cfg.q) * LAM_UNIT
+    return b
 
 
-def intrinsic_spread(cfg, oracle, problem, idx, iters, lambda_in=None, seed=0):
-    """Oracle's own spread on instances `idx` under PERT_REL perturbations of the input."""
-    P, _, _ = bpoly_basis(cfg.q, cfg.T, cfg.degree)
-    init = np.asarray(problem["init"], dtype=np.float64)[idx]
-    lam = None if lambda_in is None else np.asarray(lambda_in, np.float64)[idx]
-    base = oracle.solve(problem["bnd"], problem["obs_xy"], problem["obs_ab"], init, iters, lambda_in=lam)
-    rng = np.random.default_rng(seed)
-    st = np.zeros(len(idx))
-    sJ = np.zeros(len(idx))
-    sr = np.zeros((len(idx), 2))
-    obs = np.asarray(problem["obs_xy"], dtype=np.float64)
-    for _ in range(N_PERT):
-        pert = init.copy()
-        pert[:, :2, 3:8] *= 1.0 + PERT_REL * rng.standard_normal(pert[:, :2, 3:8].shape)
-        obs_p = obs + PERT_OBS * rng.standard_normal(obs.shape) if obs.size else obs
-        o = oracle.solve(problem["bnd"], obs_p, problem["obs_ab"], pert, iters, lambda_in=lam)
-        t_, J_, r_ = _deviations(P, o["coeffs"], base["coeffs"], o["cost"], base["cost"], o["residual"],
-                                 base["residual"])
-        st, sJ, sr = np.maximum(st, t_), np.maximum(sJ, J_), np.maximum(sr, r_)
-    return st, sJ, sr
+def fp32_spread(oracle, problem, rows, iters, ref_rows: dict, lambda_in=None, P=None,
+                seeds=None) -> dict:
+    """Largest deviation from the fp64 oracle (ref_rows) of N_MODEL fp32-model runs
+    on instances `rows` of `problem`, per quantity."""
+    from oracle import Oracle
+    if P is None:
+        P, _, _ = bpoly_basis(oracle.params.q, oracle.params.T, oracle.params.degree)
+    rows = np.asarray(rows)
+    init = np.asarray(problem["init"], np.float64)[rows]
+    lam = None if lambda_in is None else np.asarray(lambda_in, np.float64)[rows]
+    seeds = range(MODEL_SEED0, MODEL_SEED0 + N_MODEL) if seeds is None else seeds
+    spread = {}
+    for s in seeds:
+        om = Oracle(dataclasses.replace(oracle.params, fp32_model=1, noise_seed=int(s)), oracle.n)
+        m = om.solve(problem["bnd"], problem["obs_xy"], problem["obs_ab"], init, iters, lambda_in=lam)
+        for k, v in deviations(P, m, ref_rows).items():
+            spread[k] = np.maximum(spread.get(k, 0.0), v)
+    return spread
+
+
+def _take(d: dict, rows) -> dict:
+    out = {}
+    for k, v in d.items():
+        if isinstance(v, np.ndarray) and v.ndim >= 1 and k not in ("best",):
+            out[k] = v[rows]
+    return out
 
 
 def compare(cfg, gpu: dict, ref: dict, tau: float, label: str = "", check_best: bool = True,
             oracle=None, problem=None, iters=None, lambda_in=None, idx=None) -> dict:
-    """Element-by-element bar; instances that miss it are re-examined for ill-conditioning
-    when `oracle` and `problem` are given (idx maps rows to problem instances)."""
+    """Element-by-element bar; instances that miss it are re-examined with the fp32
+    rounding model when `oracle` and `problem` are given (idx maps the rows of
+    gpu / ref to instances of problem)."""
     P, _, _ = bpoly_basis(cfg.q, cfg.T, cfg.degree)
+    iters = cfg.K if iters is None else iters
+    dev = deviations(P, gpu, ref)
+    bar = bars(cfg, ref, iters)
+    n = len(dev["traj"])
+    fails = {k: dev[k] > bar[k] for k in dev if k in bar}
+    bad = np.flatnonzero(np.any(np.stack(list(fails.values())), axis=0))
     Jr = np.asarray(ref["cost"], np.float64)
-    rr = np.asarray(ref["residual"], np.float64)
-    dtraj, dJ, dr = _deviations(P, gpu["coeffs"], ref["coeffs"], gpu["cost"], Jr, gpu["residual"], rr)
-    dpsi = np.max(np.abs((np.asarray(gpu["coeffs"], np.float64)[:, 4] - ref["coeffs"][:, 4]) @ P.T), axis=1)
-    bad = np.where(_fails(cfg, dtraj, dJ, dr, Jr, rr))[0]
-    stats = dict(label=label, n=len(dtraj), max_dtraj=float(dtraj.max()), max_dpsi=float(dpsi.max()),
-                 worst_inst=int(dtraj.argmax()), max_rel_dJ=float(np.max(dJ / (np.abs(Jr) + 1e-12))),
-                 max_dr=float(dr.max()), ill_conditioned=[])
+    stats = dict(label=label, n=n, **{f"max_d{k}": float(v.max()) for k, v in dev.items()},
+                 worst_inst=int(dev["traj"].argmax()),
+                 max_rel_dJ=float(np.max(dev["cost"] / (np.abs(Jr) + 1e-12))), fp32_model_accepted=[])
     if bad.size and oracle is not None and problem is not None:
         rows = bad if idx is None else np.asarray(idx)[bad]
-        st, sJ, sr = intrinsic_spread(cfg, oracle, problem, rows, cfg.K if iters is None else iters,
-                                      lambda_in=lambda_in)
-        accept = ~_fails(cfg, dtraj[bad], dJ[bad], dr[bad], Jr[bad], rr[bad],
-                         scale=(KAPPA * st, KAPPA * sJ, KAPPA * sr))
-        for b, s_t, s_J, ok in zip(bad, st, sJ, accept):
-            if ok:
-                stats["ill_conditioned"].append(dict(inst=int(b), dtraj=float(dtraj[b]), spread_traj=float(s_t),
-                                                     dJ=float(dJ[b]), spread_J=float(s_J)))
-        bad = bad[~accept]
+        sp = fp32_spread(oracle, problem, rows, iters, _take(ref, bad), lambda_in=lambda_in, P=P)
+        keep = []
+        for i, b in enumerate(bad):
+            failing = [k for k in fails if fails[k][b]]
+            ratios = {k: float(dev[k][b] / max(sp[k][i], 1e-300)) for k in failing}
+            if all(r <= KAPPA for r in ratios.values()):
+                stats["fp32_model_accepted"].append(
+                    dict(inst=int(b), **{f"d{k}": float(dev[k][b]) for k in failing},
+                         **{f"spread_{k}": float(sp[k][i]) for k in failing},
+                         max_ratio=max(ratios.values())))
+            else:
+                keep.append((int(b), {k: (float(dev[k][b]), float(bar[k][b]), float(sp[k][i])) for k in failing}))
+        bad = np.array([b for b, _ in keep], dtype=int)
+        stats["rejected"] = keep[:10]
+    for a in stats["fp32_model_accepted"]:
+        print(f"{label}: instance {a['inst']} accepted by the fp32 rounding model: {a}")
     msg = f"{label}: {stats}; failing instances {bad.tolist()[:10]}"
     assert bad.size == 0, msg
     if check_best and "best_index" in ref:
         gb = int(np.asarray(gpu["best"])[0])
         rb = ref["best_index"]
+        stats["best"] = (gb, rb)
         if gb != rb:
-            r1 = rr[:, 0]
+            r1 = np.asarray(ref["residual"], np.float64)[:, 0]
             feas, v = key_value(r1, Jr, tau)
-            near_tau = np.any(np.abs(r1 - tau) <= 1e-3 * tau)
+            near_tau = bool(np.any(np.abs(r1 - tau) <= 1e-3 * tau))
             order = np.lexsort((np.arange(len(v)), v, ~feas))
-            ambiguous = near_tau or (len(v) > 1 and feas[order[0]] == feas[order[1]]
-                                     and abs(float(v[order[1]]) - float(v[order[0]])) <= 1e-3 * abs(float(v[order[0]])))
-            ill = {d["inst"] for d in stats["ill_conditioned"]}
-            assert ambiguous or rb in ill or gb in ill, \
-                f"{label}: best index gpu {gb} != oracle {rb} on an unambiguous scene"
+            close = (len(v) > 1 and feas[order[0]] == feas[order[1]]
+                     and abs(float(v[order[1]]) - float(v[order[0]])) <= 1e-3 * abs(float(v[order[0]])))
+            assert near_tau or close, f"{label}: best index gpu {gb} != oracle {rb} on an unambiguous scene"
+            assert feas[gb] == feas[rb] and abs(float(v[gb]) - float(v[rb])) <= 1e-4 * abs(float(v[rb])), \
+                f"{label}: ambiguous scene, but the GPU's pick {gb} is not within 1e-4 of the oracle's best {rb}"
     return stats

@@ -28,7 +28,7 @@ def lib():
 def test_header_declares_the_boundary():
     names = _declared()
     for n in ("bmc_setup", "bmc_solve", "bmc_solve_host", "bmc_destroy", "bmc_last_error", "bmc_version",
-              "bmc_last_launch_count", "bmc_sample_init", "bmc_pack_best", "bmc_select_best"):
+              "bmc_last_launch_count", "bmc_sample_init", "bmc_pack_best", "bmc_select_best", "bmc_team_for"):
         assert n in names
 
 
@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol(lib):
     raw = C.CDLL(os.path.join(ROOT, "paper_2109_13030_b200", "libbmc.so"))
     for n in _declared():
         assert hasattr(raw, n), n
-    assert lib.bmc_version() == 101
+    assert lib.bmc_version() == 102
 
 
 def _params(**kw):
@@ -70,7 +70,18 @@ def test_setup_null_arguments(lib):
     assert lib.bmc_setup(None, C.byref(h)) == 1
     assert lib.bmc_solve(None, None, None, None) == 1
     assert lib.bmc_solve_host(None, None, None) == 1
+    assert lib.bmc_team_for(None, 1000) == 0
     lib.bmc_destroy(None)
+
+
+def test_exchange_entry_points_report_errors(lib):
+    """bmc_pack_best / bmc_select_best validate before launching and set bmc_last_error."""
+    lib.bmc_last_error()
+    assert lib.bmc_pack_best(None, None, None, None, 0, None, None) == 1
+    assert "bmc_pack_best" in lib.bmc_last_error().decode()
+    buf = (C.c_int64 * 64)()
+    assert lib.bmc_select_best(buf, 0, buf, buf, None) == 1
+    assert "nranks" in lib.bmc_last_error().decode()
 
 
 def test_setup_without_gpu_fails_cleanly(lib):

@@ -43,6 +43,7 @@ def test_pack_select_equals_global_argmin():
         shard_outs.append(o)
         rec = records[r * RECORD_WORDS:(r + 1) * RECORD_WORDS]
         assert L.bmc_pack_best(C.c_void_p(o["best"].data_ptr()), C.c_void_p(o["coeffs"].data_ptr()),
+                               C.c_void_p(o["residual"].data_ptr()), C.c_void_p(o["cost"].data_ptr()),
                                C.c_int64(r * B), C.c_void_p(rec.data_ptr()), stream) == 0
     best = torch.zeros(2, dtype=torch.int64, device=dev)
     coeffs = torch.zeros(55, dtype=torch.float32, device=dev)
@@ -54,6 +55,11 @@ def test_pack_select_equals_global_argmin():
         assert torch.equal(o["coeffs"], whole["coeffs"][r * B:(r + 1) * B])
     assert int(best[0]) == int(whole["best"][0]) and int(best[1]) == int(whole["best"][1])
     assert torch.equal(coeffs, whole["coeffs"][int(best[0])].reshape(-1))
+    # the winning record carries the instance's residuals and cost (floats 55..57)
+    b = int(best[0])
+    recs = records.view(world, RECORD_WORDS)
+    win = recs[int(torch.argmin(recs[:, 0]))][1:].clone().view(torch.float32)
+    assert torch.equal(win[55:57], whole["residual"][b]) and float(win[57]) == float(whole["cost"][b])
 
 
 def test_sharded_entry_points_single_rank_nccl():
@@ -94,3 +100,55 @@ def test_sharded_entry_points_single_rank_nccl():
         assert np.array_equal(hb, best.cpu().numpy()) and np.array_equal(hc, coeffs.cpu().numpy())
     finally:
         dist.destroy_process_group()
+
+
+def test_c3_as_eight_shards_is_bitwise_the_one_gpu_solve():
+    """The bench batch (C3, B = 1000) solved as 8 shards of 125 (what 8 GPUs run), with
+    the team size of the whole batch (Solver.team_for): every instance is bitwise the
+    one-GPU solve's, and the exchange over the 8 records (plus one empty shard, key ~0)
+    returns the one-GPU global best.  With the automatic team of a 125-instance shard
+    (4 warps per instance instead of 2) the fp64 partial sums are combined in another
+    order; those shards still pick the same global best."""
+    import ctypes as C
+    from paper_2109_13030_b200 import solver_for
+    from paper_2109_13030_b200.bmc import load_library
+    from paper_2109_13030_b200.distributed import EMPTY_KEY, RECORD_WORDS
+
+    cfg = CONFIGS["C3"]
+    pr = make_problem(cfg, 0)
+    dev = torch.device("cuda", 0)
+    s = solver_for(cfg, device=0)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    obs, ab = d(pr["obs_xy"]), d(pr["obs_ab"])
+    whole = s.solve(d(pr["init"]), obs, ab, pr["bnd"], cfg.K)
+    team = s.team_for(cfg.B)
+    assert team == 2 and s.team_for(125) == 4
+    L = load_library()
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    world, per = 8, 125
+    for team_arg in (team, 0):
+        records = torch.zeros((world + 1) * RECORD_WORDS, dtype=torch.int64, device=dev)
+        outs = []
+        for r in range(world):
+            o = s.solve(d(pr["init"][r * per:(r + 1) * per]), obs, ab, pr["bnd"], cfg.K, index_base=r * per,
+                        team=team_arg)
+            outs.append(o)
+            rec = records[r * RECORD_WORDS:(r + 1) * RECORD_WORDS]
+            assert L.bmc_pack_best(C.c_void_p(o["best"].data_ptr()), C.c_void_p(o["coeffs"].data_ptr()),
+                                   None, None, C.c_int64(r * per), C.c_void_p(rec.data_ptr()), stream) == 0
+        empty = torch.tensor([0, EMPTY_KEY], dtype=torch.int64, device=dev)
+        rec = records[world * RECORD_WORDS:]
+        assert L.bmc_pack_best(C.c_void_p(empty.data_ptr()), C.c_void_p(whole["coeffs"].data_ptr()),
+                               None, None, C.c_int64(cfg.B), C.c_void_p(rec.data_ptr()), stream) == 0
+        best = torch.zeros(2, dtype=torch.int64, device=dev)
+        coeffs = torch.zeros(55, dtype=torch.float32, device=dev)
+        assert L.bmc_select_best(C.c_void_p(records.data_ptr()), world + 1, C.c_void_p(best.data_ptr()),
+                                 C.c_void_p(coeffs.data_ptr()), stream) == 0
+        torch.cuda.synchronize()
+        assert int(best[0]) == int(whole["best"][0])
+        if team_arg:
+            for r, o in enumerate(outs):
+                for k in ("coeffs", "lambda_out", "residual", "cost"):
+                    assert torch.equal(o[k], whole[k][r * per:(r + 1) * per]), (r, k)
+            assert int(best[1]) == int(whole["best"][1])
+            assert torch.equal(coeffs, whole["coeffs"][int(best[0])].reshape(-1))
