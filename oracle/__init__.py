@@ -8,10 +8,17 @@ fp64, libm), which follows PAPER.md step by step (see oracle.c's header for
 the equation map and the readings G1..G18).
 
 Parity status per function:
-  basis, KKT steps, projections, lambda step, obstacle-free fixed point,
-  invariants, worked-scene residual decay: pinned by tests/test_oracle_*.py.
-  Exact iterates on cluttered scenes: parity unpinned by the paper (it prints
-  no worked iterate); pinned only through the invariants above.
+  basis, KKT steps, projections, lambda and lambda_psi steps, cost J,
+  obstacle-free fixed point, invariants, worked-scene residual decay: pinned by
+  tests/test_oracle_*.py.  Exact iterates on cluttered scenes: parity unpinned
+  by the paper (it prints no worked iterate); pinned only through the
+  invariants above.
+
+fp32 rounding model (OracleParams.fp32_model / noise_seed, oracle.h): the same
+iteration with every quantity the product path holds in fp32 rounded where it
+is formed (stochastically when seeded).  It is a measuring instrument of the
+parity harness (tests/parity.py): how far fp32 rounding alone moves an
+instance.  Off by default; the fp64 path is unchanged by it.
 """
 from __future__ import annotations
 

@@ -669,7 +669,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
 //   U0 = n R1 e_c - D_x, U1 = (n R2 + 1) e_c - E_x, U2, U3 likewise for y,
 //   U4 = -dv_x, U5 = -da_x, U6 = -dv_y, U7 = -da_y
 // written to shared memory; D2: contraction with P, Pdot, Pddot (FP64 MMA).
-template <int M, bool RES, class WarpSmem>
+template <int M, bool RES, bool ELLK, class WarpSmem>
 __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M], WarpSmem* ws,
                                               int lane, int w, int T, int team, double (&hreg)[2],
                                               float& clkreg, PhaseClock& pc) {
@@ -782,7 +782,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     // (G18, rare: detected by the stamp reductions when culled, by a non-finite
     // sum in the plain loop) reruns the round with the guarded plain loop; one
     // call site keeps the hot loop small in the instruction cache.
-    bool general = !pa.all_cull;
+    bool general = ELLK ? !pa.all_cull : !pa.all_circ;
     bool rerun = false;   // warp-uniform: x~ = y~ = 0 exactly somewhere -> guarded pass (G18)
     if (!general) {
       float* clr = pa.clr + u * pa.nclr;
@@ -803,10 +803,10 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #endif
       BMC_SUB(pc, 13);   // culling clock and active list
       // the exact zero shows up in the stamp reductions (a round minimum r2 of 0)
-      if (pa.all_circ)
+      if (!ELLK || pa.all_circ)
         rerun = coll_circ<M, false>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
       else
-        rerun = coll_circ<M, true>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
+        rerun = coll_circ<M, ELLK>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
     }
     bool guard = false;
 #pragma unroll 1
@@ -915,7 +915,10 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #else
 #define BMC_KERNEL_BOUNDS __launch_bounds__(512)
 #endif
-template <int M, int TT>
+// ELLK: scaled-rule ellipses (alpha_rule 1) take the culled pass (coll_circ<M, true>);
+// with the literal rule (alpha_rule 0) ellipses have no zero offset outside (G8), so
+// that kernel keeps only the circle form and sends ellipse scenes to the plain loop.
+template <int M, int TT, bool ELLK>
 __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
@@ -1220,9 +1223,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       // residual terms only where they are reported: a compile-time flag keeps the
       // hot (RES = false) copy free of the per-round re-evaluation of a runtime flag
       if (want_res)
-        phase_project<M, true>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
+        phase_project<M, true, ELLK>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
       else
-        phase_project<M, false>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
+        phase_project<M, false, ELLK>(pa, r, ws, lane, w, T, team, hreg, clkreg, pc);
       __syncwarp();
       BMC_TICK(pc, 7);
       if (want_res) {   // every warp's D1 is done (barrier inside phase_project)
@@ -1329,7 +1332,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 
 // Launch of one (M, team size) kernel variant.
-template <int M, int TT>
+template <int M, int TT, bool ELLK>
 cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   // the shared-memory opt-in is per device: one bit per device ordinal (set on
   // the current device, which bmc_solve made params.device); racing threads
@@ -1339,20 +1342,20 @@ cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   const unsigned long long bit = 1ull << (dev & 63);
   if (dev >= 64 || !(attr_done.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT, ELLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
 #ifdef BMC_PROFILE
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT>) == cudaSuccess)
+    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT, ELLK>) == cudaSuccess)
       fprintf(stderr, "[bmc prof] kernel<%d,%d>: %d regs, max %d threads/block, %zu B local\n", M, TT, fa.numRegs,
               fa.maxThreadsPerBlock, fa.localSizeBytes);
 #endif
   }
   const size_t smem = smem_bytes(a.n, ipc, TT);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
-  bmc_am_kernel<M, TT><<<grid, 32 * TT * ipc, smem, s>>>(a);
+  bmc_am_kernel<M, TT, ELLK><<<grid, 32 * TT * ipc, smem, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1361,9 +1364,9 @@ cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
 template <int M>
 cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
   switch (a.team) {
-    case 1: return launch_am_mt<M, 1>(a, ipc, s);
-    case 2: return launch_am_mt<M, 2>(a, ipc, s);
-    case 4: return launch_am_mt<M, 4>(a, ipc, s);
+    case 1: return a.alpha_rule ? launch_am_mt<M, 1, true>(a, ipc, s) : launch_am_mt<M, 1, false>(a, ipc, s);
+    case 2: return a.alpha_rule ? launch_am_mt<M, 2, true>(a, ipc, s) : launch_am_mt<M, 2, false>(a, ipc, s);
+    case 4: return a.alpha_rule ? launch_am_mt<M, 4, true>(a, ipc, s) : launch_am_mt<M, 4, false>(a, ipc, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -3,24 +3,51 @@ page (--print-source sass), using an `nvdisasm -gi` listing of the same cubin.
 Each SASS instruction is attributed to the first frame of its inline chain
 (innermost first) whose bmc_kernel.cuh line falls in one of the phase ranges.
 
-usage: python tools/ncu_phases.py DIS_gi.txt SRC.csv PER [KERNEL_SUBSTR]
+usage: python tools/ncu_phases.py DIS_gi.txt SRC.csv PER [KERNEL_SUBSTR [KERNEL.cuh]]
 PER = divisor for instruction counts (e.g. B*(K+1) -> per instance-iteration)."""
 import collections, csv, re, sys
 
-RANGES = [  # (name, first, last) lines of bmc_kernel.cuh
-    ("coll", 431, 528), ("cull", 530, 565), ("B.theta", 567, 603),
-    ("D2.mma", 628, 659), ("D1.eval", 660, 718), ("D1.cullclk", 719, 746),
-    ("D1.collcall", 747, 764), ("D1.U", 765, 791), ("h.assembly", 792, 846),
-    ("prologue", 855, 1045), ("A", 1046, 1113), ("C", 1114, 1144), ("D.call", 1145, 1154),
-    ("E", 1155, 1173), ("epilogue", 1174, 1252), ("helpers", 161, 430),
+# phases as (name, first-line anchor, last-line anchor) in bmc_kernel.cuh; resolved
+# to line numbers at run time, so the attribution follows the current source
+ANCHORS = [
+    ("coll", "// Circular obstacles (coll_circ)", "// ------------------------------------------------------ temporal culling"),
+    ("cull", "// ------------------------------------------------------ temporal culling", "// ---------------------------------------------------------------- phase B"),
+    ("B.theta", "// ---------------------------------------------------------------- phase B", "// ---------------------------------------------------------------- phase D"),
+    ("D2.mma", "  const double* __restrict__ P64 = pa.Pt64;", "#pragma unroll 1\n  for (int u = T - 1 - w; u < pa.rounds; u += T)"),
+    ("D1.eval", "for (int u = T - 1 - w; u < pa.rounds; u += T)", "    BMC_SUB(pc, 12);"),
+    ("D1.cullclk", "    BMC_SUB(pc, 12);", "    bool guard = false;"),
+    ("D1.collcall", "    bool guard = false;", "    BMC_SUB(pc, 14);"),
+    ("D1.U", "    BMC_SUB(pc, 14);", "  BMC_TICK(pc, 10);"),
+    ("h.assembly", "  BMC_TICK(pc, 10);", "// ---------------------------------------------------------------- kernel"),
+    ("prologue", "// ---------------------------------------------------------------- kernel", "    for (int it = -1; it < K; ++it) {"),
+    ("A", "    for (int it = -1; it < K; ++it) {", "      // ---- B: heading target"),
+    ("C", "      // ---- B: heading target", "      // ---- D: projections"),
+    ("D.call", "      // ---- D: projections", "        // ---- E: multipliers"),
+    ("E", "        // ---- E: multipliers", "    if (lp_pending) lampsi_step();"),
+    ("epilogue", "    if (lp_pending) lampsi_step();", "size_t kernel_smem_bytes"),
 ]
+RANGES = []
+
+
+def resolve(src_path):
+    lines = open(src_path).read().split("\n")
+    def find(anchor, after=0):
+        first = anchor.split("\n")[0]
+        for i in range(after, len(lines)):
+            if first in lines[i]:
+                return i + 1
+        raise ValueError(anchor)
+    for name, a, b in ANCHORS:
+        lo = find(a)
+        hi = find(b, lo) - 1
+        RANGES.append((name, lo, hi))
 
 
 def frame_phase(chain):
     for f, ln in chain:
         if f.endswith("bmc_kernel.cuh"):
             for name, lo, hi in RANGES:
-                if lo <= ln <= hi and name != "helpers":
+                if lo <= ln <= hi:
                     return name
     return "other"
 
@@ -28,6 +55,9 @@ def frame_phase(chain):
 def main():
     dis, src, per = sys.argv[1], sys.argv[2], float(sys.argv[3])
     ksel = sys.argv[4] if len(sys.argv) > 4 else "bmc_am_kernelILi3ELi2E"
+    import os
+    resolve(sys.argv[5] if len(sys.argv) > 5 else os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "paper_2109_13030_b200", "csrc", "bmc_kernel.cuh"))
     insts, in_k, chain, fresh = [], False, [("?", 0)], True
     for l in open(dis):
         if l.strip().startswith(".section") and ".text." in l:
