@@ -231,6 +231,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mpc", action="store_true",
                     help="NEXT-1: time the receding-horizon MPC tick (P:585) instead of the C3 batch solve")
+    ap.add_argument("--ellipse", type=int, default=None, choices=[0, 1],
+                    help="NEXT-4: the same scene with elliptical obstacles under alpha rule 0 (literal) or 1 (scaled)")
     ap.add_argument("--strong", type=int, default=0, metavar="B",
                     help="strong scaling: one global batch of B instances split over the GPUs (e.g. 16384, C5)")
     args = ap.parse_args()
@@ -268,6 +270,11 @@ def main():
     # every rank builds the same scene from the seed; rank r owns instances [r B, (r+1) B)
     n_glob = cfg.B * world if global_batch is None else global_batch
     glob = make_problem(cfg, 0, B=n_glob)
+    skw = {}
+    if args.ellipse is not None:   # NEXT-4: seeded semi-axes, the chosen alpha rule
+        rng = np.random.default_rng(1000)
+        glob["obs_ab"] = np.stack([rng.uniform(0.5, 0.9, cfg.n), rng.uniform(0.35, 0.7, cfg.n)], 1).astype(np.float32)
+        skw["alpha_rule"] = args.ellipse
     shard = slice(min(rank * cfg.B, n_glob), min((rank + 1) * cfg.B, n_glob))
     init_h = np.ascontiguousarray(glob["init"][shard])
     B_rank = init_h.shape[0]
@@ -275,7 +282,7 @@ def main():
     init = torch.from_numpy(init_h).to(dev)
     obs = torch.from_numpy(glob["obs_xy"]).to(dev)
     ab = torch.from_numpy(glob["obs_ab"]).to(dev)
-    solver = solver_for(cfg, device=local)
+    solver = solver_for(cfg, device=local, **skw)
     # the team size of the whole batch on one GPU: every instance is bitwise the
     # unsharded solve's, whatever N (include/bmc.h "Determinism")
     team = solver.team_for(n_glob)
@@ -415,7 +422,9 @@ def main():
                 warmup=args.warmup, ms_per_step=1e3 * t_dev / args.steps, higher_is_better=True,
                 scaling="weak" if global_batch is None else "strong", vs_baseline=None,
                 dtype="f32 (fp64 KKT steps)", data="synthetic",
-                config=workload(cfg, world, global_batch) | {"team": team}, clocks=clocks, gpu_launches=launches,
+                config=workload(cfg, world, global_batch) | {"team": team} |
+                ({"obstacles": f"ellipses a~U(0.5,0.9) b~U(0.35,0.7), alpha rule {args.ellipse}"}
+                 if args.ellipse is not None else {}), clocks=clocks, gpu_launches=launches,
                 e2e=dict(value=e2e_value, unit="trajectories*iterations/s", h2d_bytes_per_step=int(h2d),
                          d2h_bytes_per_step=int(d2h), ms_per_step=1e3 * t_e2e / args.steps),
                 roofline=roof, wall_s=wall)

@@ -5,6 +5,9 @@
   Table VI (P:698-720): ms per iteration vs batch {5, 200, ..., 1000}
            (obstacles / circles unstated in the paper: C3's 3 x 30 here).
   C5       (BASELINE.json configs[4]): batch 100 ... 16384 at m = 3, n = 30.
+  Ellipses (NEXT-4): the C3 scene with elliptical obstacles
+           (a ~ U(0.5, 0.9), b ~ U(0.35, 0.7) m) under the literal rule (plain
+           loop) and the scaled rule (culled, and with BMC_NOCULL=1 unculled).
 
 Every point is one bmc_solve of K = 100 iterations on seeded C3-shaped dynamic
 scenes (synth.make_problem), timed with CUDA events on the launching stream
@@ -31,10 +34,19 @@ T5_N = [1, 5, 10, 15, 20, 25, 30]
 PAPER_T6 = {5: 0.0016, 200: 0.0017, 400: 0.0026, 600: 0.0033, 800: 0.0039, 1000: 0.0045}
 
 
-def time_solve(cfg, reps=10, warm=3):
+def ellipse_axes(n, seed=1000):
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.uniform(0.5, 0.9, n), rng.uniform(0.35, 0.7, n)], 1).astype(np.float32)
+
+
+def time_solve(cfg, reps=10, warm=3, alpha_rule=None):
     pr = make_problem(cfg, 0)
     d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    s = solver_for(cfg, device=0)
+    kw = {}
+    if alpha_rule is not None:   # ellipse scene
+        pr["obs_ab"] = ellipse_axes(cfg.n)
+        kw["alpha_rule"] = alpha_rule
+    s = solver_for(cfg, device=0, **kw)
     args = (d(pr["init"]), d(pr["obs_xy"]), d(pr["obs_ab"]), pr["bnd"], cfg.K)
     out = s.solve(*args)
     for _ in range(warm):
@@ -55,7 +67,8 @@ def time_solve(cfg, reps=10, warm=3):
 def main():
     torch.cuda.set_device(0)
     base = CONFIGS["C3"]
-    res = {"device": torch.cuda.get_device_name(0), "K": base.K, "table5": [], "table6": [], "c5": []}
+    res = {"device": torch.cuda.get_device_name(0), "K": base.K, "table5": [], "table6": [], "c5": [],
+           "ellipses": []}
     for m in (1, 2, 4):
         for idx, n in enumerate(T5_N):
             ms = time_solve(base.with_(m=m, n=n, B=1000))
@@ -68,6 +81,15 @@ def main():
     for B in (100, 256, 1000, 2048, 4096, 8192, 16384):
         ms = time_solve(base.with_(B=B))
         res["c5"].append({"B": B, "ms_per_solve": ms, "traj_iter_per_s": B * base.K / (ms * 1e-3)})
+    res["ellipses"].append({"scene": "C3 circles (reference)", "ms_per_solve": time_solve(base)})
+    for rule, nocull in ((0, False), (1, False), (1, True)):
+        if nocull:
+            os.environ["BMC_NOCULL"] = "1"
+        ms = time_solve(base, alpha_rule=rule)
+        os.environ.pop("BMC_NOCULL", None)
+        res["ellipses"].append({"scene": f"C3 ellipses, alpha rule {rule} ({'literal, plain loop' if rule == 0 else 'scaled'}"
+                                         f"{', unculled' if nocull else (', culled' if rule else '')})",
+                                "ms_per_solve": ms})
     if len(sys.argv) > 1:
         with open(sys.argv[1], "w") as f:
             json.dump(res, f, indent=1)
@@ -87,6 +109,10 @@ def main():
     print("| B | ms / solve | traj*iter/s |\n|---|---|---|")
     for r in res["c5"]:
         print(f"| {r['B']} | {r['ms_per_solve']:.3f} | {r['traj_iter_per_s']:.3e} |")
+    print("\n## Ellipse scenes (NEXT-4), B = 1000, K = 100\n")
+    print("| scene | ms / solve |\n|---|---|")
+    for r in res["ellipses"]:
+        print(f"| {r['scene']} | {r['ms_per_solve']:.3f} |")
 
 
 if __name__ == "__main__":
