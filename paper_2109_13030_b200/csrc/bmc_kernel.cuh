@@ -808,22 +808,18 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       else
         rerun = coll_circ<M, ELLK>(RES, ob, pa.abi, pa.ell, pa.list, na, clr, A, lane, XY, rec, res_s, D, rc) != 0u;
     }
-    bool guard = false;
-#pragma unroll 1
-    for (;;) {   // one call site of the plain loop: ellipses, and the rare guarded rerun
-      if (general || guard) coll_general<M>(RES, guard, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
-      if (guard) break;
-      if (general) {   // ellipses: a non-finite sum flags the exact zero
-        float chk = rc;
+    else {   // the plain loop (ellipses the culled pass cannot take): a non-finite sum flags the exact zero
+      coll_general<M>(RES, false, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
+      float chk = rc;
 #pragma unroll
-        for (int i = 0; i < M; ++i) chk += D[i].x + D[i].y;
-        rerun = __any_sync(FULL, !isfinite(chk));
-      }
-      if (!rerun) break;
+      for (int i = 0; i < M; ++i) chk += D[i].x + D[i].y;
+      rerun = __any_sync(FULL, !isfinite(chk));
+    }
+    if (rerun) {   // rare: redo the round with the guarded plain loop (G18)
 #pragma unroll
       for (int i = 0; i < M; ++i) D[i] = make_float2(0.f, 0.f);
       rc = 0.f;
-      guard = true;
+      coll_general<M>(RES, true, ob, pa.abi, n, 0, 1, XY, rec, res_s, D, rc);
     }
     BMC_SUB(pc, 14);   // collision projections
     float2 nDs = make_float2(0.f, 0.f), nE = nDs;   // -sum_i delta_i, -sum_i r_i delta_i
