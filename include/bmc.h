@@ -118,7 +118,9 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out);
  * is a caller-owned DEVICE pointer on params.device (contiguous, 16-byte
  * aligned); the library reads/writes them only during the stream-ordered
  * execution of this call and never frees or retains them.  The first solve
- * with a new n_obs builds and uploads that n's constants (synchronous, once).
+ * with a new n_obs builds that n's constants on the host and uploads them
+ * asynchronously on `stream`; the context keeps the constants of at most 8
+ * obstacle counts (evicting the least recently used synchronises the device).
  * Errors: BMC_EINVAL (B < 1, n or K out of range, NULL required pointer,
  * misaligned pointer), BMC_ECUDA (launch failure), BMC_ENOMEM. */
 int32_t bmc_solve(bmc_ctx* ctx, const bmc_problem* prob, const bmc_result* res,

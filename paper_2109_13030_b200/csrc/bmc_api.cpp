@@ -50,10 +50,14 @@ struct DeviceGuard {  // restore the caller's current device
 };
 
 struct Blob {
-  unsigned char* d = nullptr;
+  unsigned char* d = nullptr;   // device constants of one obstacle count
+  unsigned char* h = nullptr;   // page-locked host copy (source of the asynchronous upload)
   int nb = 0;
   int blockdiag = 0;
+  unsigned long long used = 0;  // LRU tick
 };
+
+constexpr size_t BLOB_CACHE_MAX = 8;   // obstacle counts kept per context
 
 struct HostBuf {  // context-owned device buffers for bmc_solve_host
   void* p = nullptr;
@@ -71,7 +75,8 @@ struct bmc_ctx {
   bmc_params p{};
   std::vector<double> r;
   int q = 0, QP = 0, NT = 0;
-  std::map<int, Blob> blobs;   // by n_obs
+  std::map<int, Blob> blobs;   // by n_obs, at most BLOB_CACHE_MAX (least recently used evicted)
+  unsigned long long tick = 0;
   unsigned long long* ws_key = nullptr;   // argmin workspace of bmc_solve
   unsigned int* ws_count = nullptr;
   unsigned long long* ws_key_h = nullptr; // ... and of bmc_solve_host (its own stream)
@@ -209,37 +214,60 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
 void bmc_destroy(bmc_ctx* c) {
   if (!c) return;
   DeviceGuard g(c->p.device);
-  for (auto& kv : c->blobs) cudaFree(kv.second.d);
+  for (auto& kv : c->blobs) {
+    cudaFree(kv.second.d);
+    if (kv.second.h) cudaFreeHost(kv.second.h);
+  }
   if (c->ws_key) cudaFree(c->ws_key);
   for (auto& b : c->hb) cudaFree(b.p);
   if (c->hstream) cudaStreamDestroy(c->hstream);
   delete c;
 }
 
-static int32_t get_blob(bmc_ctx* c, int n, Blob** out) {
+// Constants for obstacle count n: built on the host (fp64, setup.cpp) the first
+// time n is seen and uploaded asynchronously on the solve's stream from a
+// page-locked copy the context keeps.  At most BLOB_CACHE_MAX counts are kept;
+// evicting the least recently used one synchronises the device first (a solve
+// on another stream may still read it), which only happens when more than
+// BLOB_CACHE_MAX distinct counts are in use.
+static int32_t get_blob(bmc_ctx* c, int n, cudaStream_t stream, Blob** out) {
   auto it = c->blobs.find(n);
   if (it != c->blobs.end()) {
+    it->second.used = ++c->tick;
     *out = &it->second;
     return BMC_OK;
   }
   HostConsts hc;
   std::string err;
   if (build_consts(setup_params(c), n, &hc, &err) != 0) return fail(BMC_ESINGULAR, err);
+  cudaError_t e;
+  if (c->blobs.size() >= BLOB_CACHE_MAX) {
+    auto lru = c->blobs.begin();
+    for (auto jt = c->blobs.begin(); jt != c->blobs.end(); ++jt)
+      if (jt->second.used < lru->second.used) lru = jt;
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize(blob eviction)");
+    cudaFree(lru->second.d);
+    cudaFreeHost(lru->second.h);
+    c->blobs.erase(lru);
+  }
   Blob b;
   b.nb = hc.nb;
   b.blockdiag = hc.blockdiag;
+  b.used = ++c->tick;
   const size_t bytes = BlobLayout::bytes(hc.QP);
-  cudaError_t e = cudaMalloc(&b.d, bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(blob)");
-  std::vector<unsigned char> host(bytes);
-  std::memcpy(host.data(), hc.blob_f64, BlobLayout::bytes_f64);
-  std::memcpy(host.data() + BlobLayout::bytes_f64, hc.pt, BlobLayout::bytes_f32(hc.QP));
-  std::memcpy(host.data() + BlobLayout::bytes_f64 + BlobLayout::bytes_f32(hc.QP), hc.pt64,
-              BlobLayout::bytes_p64(hc.QP));
-  e = cudaMemcpy(b.d, host.data(), bytes, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
+  if ((e = cudaHostAlloc(reinterpret_cast<void**>(&b.h), bytes, cudaHostAllocDefault)) != cudaSuccess)
+    return cuda_fail(e, "cudaHostAlloc(blob)");
+  std::memcpy(b.h, hc.blob_f64, BlobLayout::bytes_f64);
+  std::memcpy(b.h + BlobLayout::bytes_f64, hc.pt, BlobLayout::bytes_f32(hc.QP));
+  std::memcpy(b.h + BlobLayout::bytes_f64 + BlobLayout::bytes_f32(hc.QP), hc.pt64, BlobLayout::bytes_p64(hc.QP));
+  if ((e = cudaMalloc(&b.d, bytes)) != cudaSuccess) {
+    cudaFreeHost(b.h);
+    return cuda_fail(e, "cudaMalloc(blob)");
+  }
+  if ((e = cudaMemcpyAsync(b.d, b.h, bytes, cudaMemcpyHostToDevice, stream)) != cudaSuccess) {
     cudaFree(b.d);
-    return cuda_fail(e, "cudaMemcpy(blob)");
+    cudaFreeHost(b.h);
+    return cuda_fail(e, "cudaMemcpyAsync(blob)");
   }
   c->blobs[n] = b;
   *out = &c->blobs[n];
@@ -318,7 +346,7 @@ int32_t bmc_team_for(const bmc_ctx* c, int64_t B) {
 static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, cudaStream_t s,
                           unsigned long long* ws_key, unsigned int* ws_count) {
   Blob* blob = nullptr;
-  int32_t rc = get_blob(c, pr->n_obs, &blob);
+  int32_t rc = get_blob(c, pr->n_obs, s, &blob);
   if (rc != BMC_OK) return rc;
   int ipc = 1, team = 1;
   launch_shape(c, pr->B, pr->team, &ipc, &team);
