@@ -127,14 +127,15 @@ def test_c3_full_batch_every_instance(seed):
     assert len(st["fp32_model_accepted"]) <= 50      # <= 5 % rely on the model (3-5 % measured, mostly lambda)
 
 
-def test_c4_full_batch_every_instance():
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c4_full_batch_every_instance(seed):
     """C4 (B = 1000, 4 circles, 50 obstacles, tight bounds, K = 200): every instance and the
-    best index vs the oracle (about 1-2 min of oracle time on 16 cores)."""
+    best index vs the oracle (about 1-2 min of oracle time on 16 cores per seed)."""
     cfg = CONFIGS["C4"]
-    pr = make_problem(cfg, 0)
+    pr = make_problem(cfg, seed)
     g = run_gpu(cfg, pr)
     r = run_oracle(cfg, pr)
-    st = compare(cfg, g, r, cfg.res_tol, "C4 B=1000 seed 0 all", oracle=Oracle(oracle_params(cfg), cfg.n),
+    st = compare(cfg, g, r, cfg.res_tol, f"C4 B=1000 seed {seed} all", oracle=Oracle(oracle_params(cfg), cfg.n),
                  problem=pr)
     print({k: v for k, v in st.items() if k != "fp32_model_accepted"}, len(st["fp32_model_accepted"]))
     assert len(st["fp32_model_accepted"]) <= 150     # C4: chaotic infeasible orbits (DESIGN.md "Conditioning")
@@ -460,3 +461,16 @@ def test_ellipse_culling_is_exact(monkeypatch):
     full = run_gpu(cfg, pr, solver=s)
     for k in culled:
         assert np.array_equal(culled[k], full[k]), k
+
+
+def test_ellipse_scene_full_batch_every_instance_scaled_rule():
+    """The scaled-rule ellipse scene in the culled fast path (NEXT-4): every instance of
+    B = 1000 and the best index vs the oracle."""
+    cfg = CONFIGS["C3"]
+    pr = _ellipse_scene(cfg, 5)
+    g = run_gpu(cfg, pr, alpha_rule=1)
+    r = run_oracle(cfg, pr, alpha_rule=1)
+    st = compare(cfg, g, r, cfg.res_tol, "ellipses rule 1 B=1000 all",
+                 oracle=Oracle(oracle_params(cfg, alpha_rule=1), cfg.n), problem=pr)
+    print({k: v for k, v in st.items() if k != "fp32_model_accepted"}, len(st["fp32_model_accepted"]))
+    assert len(st["fp32_model_accepted"]) <= 50
