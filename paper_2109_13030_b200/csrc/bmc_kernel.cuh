@@ -477,9 +477,10 @@ __device__ __forceinline__ bool coll_block(const bool RES, const float2* __restr
     const unsigned mn = __reduce_min_sync(FULL, __float_as_uint(r2m[jj]));
     qm = (lane == jj) ? mn : qm;
   }
-  if (lane < NB) {
-    const int j = list[jb + lane];
-    clr[j] = sqrt_approx(__uint_as_float(qm)) - (ELL ? ell[j].z : abi[j].x) * 1.00001f + A;
+  {   // lanes < NB stamp their obstacle (predicated store, no divergent block)
+    const int j = list[jb + min(lane, NB - 1)];
+    const float v = sqrt_approx(__uint_as_float(qm)) - (ELL ? ell[j].z : abi[j].x) * 1.00001f + A;
+    if (lane < NB) clr[j] = v;
   }
   return qm == 0u;
 }
@@ -877,7 +878,8 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
   // team's partials in warp order and assemble
   //   h_pos  = P^T U0 + Dm^T (P^T U4) + Dm^T Dm^T (P^T U5)   (x; y: U2, U6, U7)
   //   h_copy = P^T U1                                          (x; y: U3)
-  const int nch = (T == 1) ? 2 : (w < 2 ? 1 : 0);
+  // channels owned (compile-time for teams of 1 and 2: no branch)
+  const int nch = (T == 1) ? 2 : (T == 2 ? 1 : (w < 2 ? 1 : 0));
   const int k = lane;
 #pragma unroll
   for (int ci = 0; ci < 2; ++ci) {   // unrolled: hreg stays in registers
@@ -1071,7 +1073,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     const double rho = a.rho, rho_psi = a.rho_psi;
     const double* dmtab = ub + DM_TAB;
     // channels owned by this warp (phases A, D2, E): both for T = 1, channel w for w < 2
-    const int nown = (T == 1) ? 2 : (w < 2 ? 1 : 0);
+    const int nown = (T == 1) ? 2 : (T == 2 ? 1 : (w < 2 ? 1 : 0));   // compile-time for T <= 2
     const int chb = (T == 1) ? 0 : w;
     double xi[2] = {0.0, 0.0}, lam[2] = {0.0, 0.0}, cref[2] = {0.0, 0.0};
     double hreg[2] = {0.0, 0.0};   // h = F^T (F xi1 - g) of the owned channels, lane k: entry k (phase D2)
