@@ -916,7 +916,9 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 // ELLK: scaled-rule ellipses (alpha_rule 1) take the culled pass (coll_circ<M, true>);
 // with the literal rule (alpha_rule 0) ellipses have no zero offset outside (G8), so
 // that kernel keeps only the circle form and sends ellipse scenes to the plain loop.
-template <int M, int TT, bool ELLK>
+// BD: M and K11 block diagonal (symmetric footprint, sum r_i = 0: every configured
+// one); a compile-time branch, so the common kernel carries only its mat-vec.
+template <int M, int TT, bool ELLK, bool BD>
 __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
@@ -1139,7 +1141,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           // symmetric footprint M and K11 are block diagonal (setup.cpp): row k only
           // meets the columns of its own block (c_x rows 0..10, c_c rows 11..21).
           double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-          if (a.blockdiag) {
+          if (BD) {
             const int j0 = (kc < NV) ? 0 : NV;
 #pragma unroll
             for (int jj = 0; jj < NV; ++jj) {
@@ -1170,13 +1172,16 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           // n = 10; lanes >= 11 hold the copy block and meet zero weights)
           const double d1 = dm_apply(xi[c], dmtab, k);
           const double d2 = dm_apply(d1, dmtab, k);
+          // predicated stores (no divergent block): lanes k < 11 the position block,
+          // lanes 11..21 the copy block
+          const int kp = min(k, NV - 1), kq = min(max(k - NV, 0), NV - 1);
+          const float xf = (float)(xi[c] - cref[c]), d1f = (float)d1, d2f = (float)d2, cf = (float)xi[c];
           if (k < NV) {
-            ws->cfi[k][ch] = (float)(xi[c] - cref[c]);
-            ws->cfi[k][2 + ch] = (float)d1;
-            ws->cfi[k][4 + ch] = (float)d2;
-          } else if (k < NV2) {
-            ws->cfi[k - NV][6 + ch] = (float)xi[c];
+            ws->cfi[kp][ch] = xf;
+            ws->cfi[kp][2 + ch] = d1f;
+            ws->cfi[kp][4 + ch] = d2f;
           }
+          if (k >= NV && k < NV2) ws->cfi[kq][6 + ch] = cf;
         }
         if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
@@ -1330,7 +1335,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 
 // Launch of one (M, team size) kernel variant.
-template <int M, int TT, bool ELLK>
+template <int M, int TT, bool ELLK, bool BD>
 cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   // the shared-memory opt-in is per device: one bit per device ordinal (set on
   // the current device, which bmc_solve made params.device); racing threads
@@ -1340,21 +1345,28 @@ cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   const unsigned long long bit = 1ull << (dev & 63);
   if (dev >= 64 || !(attr_done.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT, ELLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT, ELLK, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
 #ifdef BMC_PROFILE
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT, ELLK>) == cudaSuccess)
+    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT, ELLK, BD>) == cudaSuccess)
       fprintf(stderr, "[bmc prof] kernel<%d,%d>: %d regs, max %d threads/block, %zu B local\n", M, TT, fa.numRegs,
               fa.maxThreadsPerBlock, fa.localSizeBytes);
 #endif
   }
   const size_t smem = smem_bytes(a.n, ipc, TT);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
-  bmc_am_kernel<M, TT, ELLK><<<grid, 32 * TT * ipc, smem, s>>>(a);
+  bmc_am_kernel<M, TT, ELLK, BD><<<grid, 32 * TT * ipc, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int M, int TT>
+cudaError_t launch_am_t(const KernelArgs& a, int ipc, cudaStream_t s) {
+  if (a.blockdiag)
+    return a.alpha_rule ? launch_am_mt<M, TT, true, true>(a, ipc, s) : launch_am_mt<M, TT, false, true>(a, ipc, s);
+  return a.alpha_rule ? launch_am_mt<M, TT, true, false>(a, ipc, s) : launch_am_mt<M, TT, false, false>(a, ipc, s);
 }
 
 // One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
@@ -1362,9 +1374,9 @@ cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
 template <int M>
 cudaError_t launch_am_m(const KernelArgs& a, int ipc, cudaStream_t s) {
   switch (a.team) {
-    case 1: return a.alpha_rule ? launch_am_mt<M, 1, true>(a, ipc, s) : launch_am_mt<M, 1, false>(a, ipc, s);
-    case 2: return a.alpha_rule ? launch_am_mt<M, 2, true>(a, ipc, s) : launch_am_mt<M, 2, false>(a, ipc, s);
-    case 4: return a.alpha_rule ? launch_am_mt<M, 4, true>(a, ipc, s) : launch_am_mt<M, 4, false>(a, ipc, s);
+    case 1: return launch_am_t<M, 1>(a, ipc, s);
+    case 2: return launch_am_t<M, 2>(a, ipc, s);
+    case 4: return launch_am_t<M, 4>(a, ipc, s);
   }
   return cudaErrorInvalidValue;
 }
