@@ -15,8 +15,8 @@ ANCHORS = [
     ("B.theta", "// ---------------------------------------------------------------- phase B", "// ---------------------------------------------------------------- phase D"),
     ("D2.mma", "  const double* __restrict__ P64 = pa.Pt64;", "#pragma unroll 1\n  for (int u = T - 1 - w; u < pa.rounds; u += T)"),
     ("D1.eval", "for (int u = T - 1 - w; u < pa.rounds; u += T)", "    BMC_SUB(pc, 12);"),
-    ("D1.cullclk", "    BMC_SUB(pc, 12);", "    bool guard = false;"),
-    ("D1.collcall", "    bool guard = false;", "    BMC_SUB(pc, 14);"),
+    ("D1.cullclk", "    BMC_SUB(pc, 12);", "    else {   // the plain loop"),
+    ("D1.collcall", "    else {   // the plain loop", "    BMC_SUB(pc, 14);"),
     ("D1.U", "    BMC_SUB(pc, 14);", "  BMC_TICK(pc, 10);"),
     ("h.assembly", "  BMC_TICK(pc, 10);", "// ---------------------------------------------------------------- kernel"),
     ("prologue", "// ---------------------------------------------------------------- kernel", "    for (int it = -1; it < K; ++it) {"),
