@@ -200,6 +200,14 @@ __device__ __forceinline__ double f2d(float x) {
   asm("cvt.f64.f32 %0, %1;" : "=d"(d) : "f"(x));
   return d;
 }
+// fp64 -> fp32, round to nearest, without the -ftz flush of fp32 denormals (ptxas
+// emulates that flush with a compare and a multiply after every conversion); the
+// converted quantities never lie in the fp32 denormal range except 0
+__device__ __forceinline__ float d2f(double x) {
+  float f;
+  asm("cvt.rn.f32.f64 %0, %1;" : "=f"(f) : "d"(x));
+  return f;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT, ~1 ulp
   float y;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -983,8 +991,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     float2 v = make_float2(1.0e4f, 1.0e4f);
     if (t < q && j < n) {
       const double tau = (double)t * inv_q1;
-      v = make_float2((float)((double)__ldg(a.obs_xy + (size_t)(2 * j) * q + t) - fma(a.ref_dx, tau, a.ref_x0)),
-                      (float)((double)__ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t) - fma(a.ref_dy, tau, a.ref_y0)));
+      v = make_float2(d2f((double)__ldg(a.obs_xy + (size_t)(2 * j) * q + t) - fma(a.ref_dx, tau, a.ref_x0)),
+                      d2f((double)__ldg(a.obs_xy + (size_t)(2 * j + 1) * q + t) - fma(a.ref_dy, tau, a.ref_y0)));
     }
     obs[idx] = v;
   }
@@ -1106,7 +1114,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       const double v = lamp - (((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth_prev);
       lamp = (k < NV) ? v : 0.0;
     };
-    if (k < NV) { ws->cf4[w][k] = (float)xi2r; ws->xi2w[w][k] = xi2r; }
+    if (k < NV) { ws->cf4[w][k] = d2f(xi2r); ws->xi2w[w][k] = xi2r; }
 
     float r1sq = 0.f, rpsq = 0.f;
     const bool trace = a.res_trace != nullptr;
@@ -1175,11 +1183,11 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           // predicated stores (no divergent block): lanes k < 11 the position block,
           // lanes 11..21 the copy block
           const int kp = min(k, NV - 1), kq = min(max(k - NV, 0), NV - 1);
-          const float xf = (float)(xi[c] - cref[c]), d1f = (float)d1, d2f = (float)d2, cf = (float)xi[c];
+          const float xf = d2f(xi[c] - cref[c]), d1f = d2f(d1), d2ff = d2f(d2), cf = d2f(xi[c]);
           if (k < NV) {
             ws->cfi[kp][ch] = xf;
             ws->cfi[kp][2 + ch] = d1f;
-            ws->cfi[kp][4 + ch] = d2f;
+            ws->cfi[kp][4 + ch] = d2ff;
           }
           if (k >= NV && k < NV2) ws->cfi[kq][6 + ch] = cf;
         }
@@ -1213,7 +1221,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           xi2r = (k < NV) ? v : 0.0;
           if (k < NV) {
             ws->xi2w[w][k] = xi2r;
-            ws->cf4[w][k] = (float)xi2r;
+            ws->cf4[w][k] = d2f(xi2r);
           }
         }
         pth_prev = pth;        // the lambda_psi step runs in the next phase A
