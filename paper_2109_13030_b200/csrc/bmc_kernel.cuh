@@ -600,11 +600,9 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
   float2 ccs[NV];   // (c_c, c_s) per Bernstein index
 #pragma unroll
   for (int k = 0; k < NV; ++k) ccs[k] = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
-#ifndef BMC_THETA_MMA
   double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-#endif
   const int nr = (q + 31) >> 5;
 #pragma unroll 2
   for (int uu = 0; uu < QP / 32; ++uu) {   // two rounds in flight: independent atan2 chains
@@ -620,56 +618,15 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     const float tht = atan2_fast(cs.y, cs.x);   // atan2(0, 0) = 0 (G18)
     ws->cs[t] = cs;
     ws->th[t] = tht;
-#ifndef BMC_THETA_MMA
     const double thd = f2d(tht);
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
-#endif
   }
-#ifndef BMC_THETA_MMA
   // 11 entries as 8 + 4 transpose-reduce slots
   const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
   const double v4 = tr_reduce<4>(acc + 8, lane);    // entry 8 + (lane >> 3)
   if (!(lane & 3)) ws->part_th[w][lane >> 2] = v8;
   if (!(lane & 7) && 8 + (lane >> 3) < NV) ws->part_th[w][8 + (lane >> 3)] = v4;
-#else
-  // P^T theta on the FP64 tensor cores: G = P^T [theta .. theta] (every column the
-  // same; column 0 is kept), k = 4 samples per m8n8k4 step, the basis as the A
-  // fragment (as in D2), theta of the warp's rounds as the B fragment
-  __syncwarp();   // the rounds' theta are in shared memory
-  const int aoff0 = (lane >> 2) * QP64 + (lane & 3), aoff1 = min(8 + (lane >> 2), NV - 1) * QP64 + (lane & 3);
-  const float* __restrict__ thc = &ws->th[lane & 3];
-  double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0}, e0[2] = {0.0, 0.0}, e1[2] = {0.0, 0.0};
-#pragma unroll 1
-  for (int u = T - 1 - w; u < nr; u += T) {
-    const int t0 = 32 * u;
-    if (t0 + 32 <= q) {
-#pragma unroll
-      for (int st = 0; st < 8; ++st) {
-        const double b = f2d(thc[t0 + 4 * st]);
-        if (st & 1) {
-          mma_f64_884(e0, Pt64[aoff0 + t0 + 4 * st], b);
-          mma_f64_884(e1, Pt64[aoff1 + t0 + 4 * st], b);
-        } else {
-          mma_f64_884(g0, Pt64[aoff0 + t0 + 4 * st], b);
-          mma_f64_884(g1, Pt64[aoff1 + t0 + 4 * st], b);
-        }
-      }
-    } else {
-      const int ns = (q - t0 + 3) >> 2;
-#pragma unroll 1
-      for (int st = 0; st < ns; ++st) {
-        const double b = f2d(thc[t0 + 4 * st]);
-        mma_f64_884(g0, Pt64[aoff0 + t0 + 4 * st], b);
-        mma_f64_884(g1, Pt64[aoff1 + t0 + 4 * st], b);
-      }
-    }
-  }
-  if (!(lane & 3)) {
-    ws->part_th[w][lane >> 2] = g0[0] + e0[0];
-    if (8 + (lane >> 2) < NV) ws->part_th[w][8 + (lane >> 2)] = g1[0] + e1[0];
-  }
-#endif
 }
 
 // ---------------------------------------------------------------- phase D
