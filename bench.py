@@ -233,6 +233,8 @@ def main():
                     help="NEXT-1: time the receding-horizon MPC tick (P:585) instead of the C3 batch solve")
     ap.add_argument("--ellipse", type=int, default=None, choices=[0, 1],
                     help="NEXT-4: the same scene with elliptical obstacles under alpha rule 0 (literal) or 1 (scaled)")
+    ap.add_argument("--team-of-batch", action="store_true",
+                    help="run every shard with the team size of the whole batch (bitwise the one-GPU solve)")
     ap.add_argument("--strong", type=int, default=0, metavar="B",
                     help="strong scaling: one global batch of B instances split over the GPUs (e.g. 16384, C5)")
     args = ap.parse_args()
@@ -283,9 +285,10 @@ def main():
     obs = torch.from_numpy(glob["obs_xy"]).to(dev)
     ab = torch.from_numpy(glob["obs_ab"]).to(dev)
     solver = solver_for(cfg, device=local, **skw)
-    # the team size of the whole batch on one GPU: every instance is bitwise the
-    # unsharded solve's, whatever N (include/bmc.h "Determinism")
-    team = solver.team_for(n_glob)
+    # team size (warps per instance): the one this shard's size selects, as each GPU
+    # would run it alone (`--team-of-batch`: the whole batch's, which makes every
+    # instance bitwise the one-GPU solve's at the cost of a smaller team per shard)
+    team = solver.team_for(n_glob) if args.team_of_batch else solver.team_for(B_rank)
     xchg = BestExchange(pg, dev) if world > 1 else None
     out = solver.solve(init, obs, ab, glob["bnd"], cfg.K, index_base=rank * cfg.B, team=team)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
