@@ -111,7 +111,10 @@ typedef struct {
 /* Build the context: Bernstein basis, boundary rows, per-channel KKT
  * inverses in fp64 (Eq. 3-4 "constant" inverse).  The device is
  * params->device.  Returns BMC_EINVAL (bad parameter, message says which),
- * BMC_ESINGULAR, BMC_ECUDA or BMC_ENOMEM; *out is NULL on error. */
+ * BMC_ESINGULAR (the KKT is singular even with an obstacle), BMC_ECUDA or
+ * BMC_ENOMEM; *out is NULL on error.  The KKT depends on n_obs through F^T F:
+ * bmc_solve returns BMC_ESINGULAR for an n_obs that makes it singular (n_obs = 0
+ * with no position row in boundary_mask). */
 int32_t bmc_setup(const bmc_params* params, bmc_ctx** out);
 
 /* Device solve, asynchronous on `stream`.  Every pointer in `prob` and `res`
@@ -122,7 +125,8 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out);
  * asynchronously on `stream`; the context keeps the constants of at most 8
  * obstacle counts (evicting the least recently used synchronises the device).
  * Errors: BMC_EINVAL (B < 1, n or K out of range, NULL required pointer,
- * misaligned pointer), BMC_ECUDA (launch failure), BMC_ENOMEM. */
+ * misaligned pointer), BMC_ESINGULAR (the KKT of this n_obs is singular),
+ * BMC_ECUDA (launch failure), BMC_ENOMEM. */
 int32_t bmc_solve(bmc_ctx* ctx, const bmc_problem* prob, const bmc_result* res,
                   bmc_stream_t stream);
 

@@ -162,7 +162,10 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
   *out = nullptr;
   int32_t rc = validate_params(params);
   if (rc != BMC_OK) return rc;
-  // singularity of the boundary / KKT does not depend on n: check it now
+  // the boundary rows and the KKT with one obstacle are checked now; the KKT of
+  // a given n is checked when that n is first solved (with no obstacle and no
+  // position row among the boundary rows it is singular: a constant shift of x
+  // changes nothing the cost or the constraints see)
   bmc_ctx* c = new (std::nothrow) bmc_ctx();
   if (!c) return fail(BMC_ENOMEM, "host allocation failed");
   c->p = *params;
@@ -174,7 +177,7 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
   {
     HostConsts hc;
     std::string err;
-    if (build_consts(setup_params(c), 0, &hc, &err) != 0) {
+    if (build_consts(setup_params(c), 1, &hc, &err) != 0) {
       delete c;
       return fail(BMC_ESINGULAR, err);
     }

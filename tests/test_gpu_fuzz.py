@@ -1,0 +1,88 @@
+"""Seeded random sweep of the ABI's parameter space, GPU (libbmc.so through the C-ABI)
+against the fp64 oracle with the full parity harness (tests/parity.py).
+
+Each case draws, from its own seed: the horizon q (11..128, so 1..4 rounds of 32
+samples, ragged tails), the footprint (1..8 circles, symmetric or not -- the
+block-diagonal and the general xi1 kernels), the obstacle count (0..64) and
+shapes (circles or ellipses under either alpha rule, G8), bounds (loose or
+tight), the weights rho, rho_psi, w_copy (G5, G10, G14), the boundary mask (G11),
+the iteration count (0..40), the batch (1..300), the team size (0 = automatic, 1,
+2, 4) and a warm or cold start.  A mask that leaves the KKT singular must be
+refused by both sides (BMC_ESINGULAR / the oracle's error).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import Oracle  # noqa: E402
+from synth import CONFIGS, make_problem  # noqa: E402
+from tests.helpers import oracle_params  # noqa: E402
+from tests.parity import compare  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MASKS = [0x3F, 0x09, 0x1B, 0x07, 0x38, 0x0F, 0x2D, 0x01, 0x08, 0x00]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def _case(seed):
+    rng = np.random.default_rng(9000 + seed)
+    q = int(rng.choice([11, 20, 32, 33, 50, 64, 77, 96, 100, 128]))
+    m = int(rng.integers(1, 9))
+    if rng.random() < 0.5:
+        r = list(np.round(np.linspace(-0.3 * (m - 1), 0.3 * (m - 1), m), 6)) if m > 1 else [0.0]
+    else:
+        r = list(np.round(rng.uniform(-0.8, 0.8, m), 4))
+    n = int(rng.choice([0, 1, 3, 5, 12, 30, 33, 64]))
+    tight = rng.random() < 0.4
+    cfg = CONFIGS["C2"].with_(q=q, m=m, n=n, B=int(rng.choice([1, 7, 37, 148, 300])),
+                              K=int(rng.choice([0, 1, 5, 20, 40])),
+                              v_max=1.2 if tight else 2.0, a_max=0.5 if tight else 2.0,
+                              rho=float(rng.choice([1.0, 0.5, 2.0])), rho_psi=float(rng.choice([1.0, 2.0, 0.7])))
+    kw = dict(r=r, w_copy=float(rng.choice([0.0, 0.0, 0.1])), boundary_mask=int(rng.choice(MASKS)),
+              alpha_rule=int(rng.integers(0, 2)))
+    ellipses = n > 0 and rng.random() < 0.35
+    team = int(rng.choice([0, 0, 1, 2, 4]))
+    warm = rng.random() < 0.3
+    return cfg, kw, ellipses, team, warm, rng
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_configuration(seed):
+    from paper_2109_13030_b200 import BmcError, solver_for
+    cfg, kw, ellipses, team, warm, rng = _case(seed)
+    pr = make_problem(cfg, 30 + seed)
+    if ellipses:
+        pr["obs_ab"] = np.stack([rng.uniform(0.4, 0.9, cfg.n), rng.uniform(0.3, 0.8, cfg.n)], 1).astype(np.float32)
+    label = f"fuzz {seed}: q={cfg.q} m={cfg.m} n={cfg.n} B={cfg.B} K={cfg.K} {kw} ell={ellipses} team={team} warm={warm}"
+    try:
+        o = Oracle(oracle_params(cfg, **kw), cfg.n)
+    except ValueError:
+        o = None
+    s = solver_for(cfg, device=0, **kw)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    if o is None:   # singular KKT for this n (e.g. no obstacle and no position row): refused
+        with pytest.raises(BmcError) as e:
+            s.solve(d(pr["init"]), d(pr["obs_xy"]) if cfg.n else None, d(pr["obs_ab"]) if cfg.n else None,
+                    pr["bnd"], cfg.K)
+        assert e.value.code == 2, label
+        return
+    lam = None
+    if warm:
+        lam = o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"], 5)["lambda_out"].astype(np.float32)
+    out = s.solve(d(pr["init"]), d(pr["obs_xy"]) if cfg.n else None, d(pr["obs_ab"]) if cfg.n else None, pr["bnd"],
+                  cfg.K, lambda_in=None if lam is None else d(lam), team=team)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    r = o.solve(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"], cfg.K, lambda_in=lam)
+    st = compare(cfg, g, r, cfg.res_tol, label, oracle=o, problem=pr, lambda_in=lam)
+    print(label, {k: v for k, v in st.items() if k.startswith("max_d")}, len(st["fp32_model_accepted"]))
