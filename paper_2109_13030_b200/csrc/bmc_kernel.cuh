@@ -82,6 +82,7 @@ struct alignas(16) WarpSmemT {
   float ppsi[QP];
   float clk[T_MAX];             // per-round movement clocks (culling)
   float pad_[T_MAX];
+  double thsum[TT >= 2 ? QP : 2];   // FM: sum over the iterations of theta per sample (lambda_psi output)
 };
 static_assert(sizeof(WarpSmemT<1>) % 16 == 0 && sizeof(WarpSmemT<2>) % 16 == 0 && sizeof(WarpSmemT<4>) % 16 == 0,
               "WarpSmem must keep 16-byte alignment");
@@ -594,15 +595,23 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
 // ---------------------------------------------------------------- phase B
 // c, s at every sample, theta = atan2(s, c) (Eq. 19; G18) into the
 // warp's smem arrays, and the warp total of P^T theta into ws->pth[0..10].
-template <class WarpSmem>
+// FM (all six boundary rows, P:269 / G11): the rows pin c_psi[0..2] and c_psi[8..10]
+// (position, velocity and acceleration at both ends involve only those
+// coefficients), so the heading step's KKT inverse Kp11 = Z (Z^T H Z)^-1 Z^T with
+// Z = [e3 .. e7] vanishes outside rows / columns 3..7: xi2 needs only the entries
+// 3..7 of P^T theta.  The other six enter only lambda_psi's boundary components,
+// which feed nothing until the output: their theta terms are summed per sample
+// over the iterations (thsum) and contracted once at the end.
+template <bool FM, class WarpSmem>
 __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
-                                            WarpSmem* ws, int lane, int q, int w, int T) {
+                                            WarpSmem* ws, int lane, int q, int w, int T, bool sum_theta) {
   float2 ccs[NV];   // (c_c, c_s) per Bernstein index
 #pragma unroll
   for (int k = 0; k < NV; ++k) ccs[k] = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
-  double acc[16];   // P^T theta in fp64 (exact products, no cancellation loss)
+  constexpr int NA = FM ? 5 : 16;
+  double acc[NA];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+  for (int k = 0; k < NA; ++k) acc[k] = 0.0;
   const int nr = (q + 31) >> 5;
 #pragma unroll 2
   for (int uu = 0; uu < QP / 32; ++uu) {   // two rounds in flight: independent atan2 chains
@@ -619,14 +628,48 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     ws->cs[t] = cs;
     ws->th[t] = tht;
     const double thd = f2d(tht);
+    if constexpr (FM) {
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
+      for (int j = 0; j < 5; ++j) acc[j] = fma(Pt64[(3 + j) * QP64 + t], thd, acc[j]);
+      if (sum_theta) ws->thsum[t] += thd;
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = fma(Pt64[k * QP64 + t], thd, acc[k]);
+    }
   }
-  // 11 entries as 8 + 4 transpose-reduce slots
-  const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
-  const double v4 = tr_reduce<4>(acc + 8, lane);    // entry 8 + (lane >> 3)
-  if (!(lane & 3)) ws->part_th[w][lane >> 2] = v8;
-  if (!(lane & 7) && 8 + (lane >> 3) < NV) ws->part_th[w][8 + (lane >> 3)] = v4;
+  if constexpr (FM) {
+    // entries 3..6 as 4 transpose-reduce slots, entry 7 as a butterfly sum: the
+    // lane bits pair in the same order as below, so the entries are bitwise the same
+    const double v4 = tr_reduce<4>(acc, lane);       // entry 3 + (lane >> 3)
+    const double v1 = warp_sum(acc[4]);              // entry 7
+    if (!(lane & 7)) ws->part_th[w][3 + (lane >> 3)] = v4;
+    if (lane == 0) ws->part_th[w][7] = v1;
+  } else {
+    // 11 entries as 8 + 4 transpose-reduce slots
+    const double v8 = tr_reduce<8>(acc, lane);        // entry lane >> 2
+    const double v4 = tr_reduce<4>(acc + 8, lane);    // entry 8 + (lane >> 3)
+    if (!(lane & 3)) ws->part_th[w][lane >> 2] = v8;
+    if (!(lane & 7) && 8 + (lane >> 3) < NV) ws->part_th[w][8 + (lane >> 3)] = v4;
+  }
+}
+
+// FM, end of the solve: the boundary components k in {0, 1, 2, 8, 9, 10} of
+// rho_psi sum_it P^T theta_it (from thsum), summed over the team into part_th[w][k].
+template <class WarpSmem>
+__device__ __forceinline__ void theta_sum_boundary(const double* __restrict__ Pt64, WarpSmem* ws, int lane, int q,
+                                                   int w, int T) {
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int nr = (q + 31) >> 5;
+#pragma unroll 1
+  for (int u = T - 1 - w; u < nr; u += T) {
+    const int t = 32 * u + lane;
+    const double ts = ws->thsum[t];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i] = fma(Pt64[(i < 3 ? i : i + 5) * QP64 + t], ts, acc[i]);
+  }
+  const double v8 = tr_reduce<8>(acc, lane);   // slot lane >> 2: k = slot (< 3) or slot + 5
+  const int slot = lane >> 2;
+  if (!(lane & 3) && slot < 6) ws->part_th[w][slot < 3 ? slot : slot + 5] = v8;
 }
 
 // ---------------------------------------------------------------- phase D
@@ -883,7 +926,7 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 // that kernel keeps only the circle form and sends ellipse scenes to the plain loop.
 // BD: M and K11 block diagonal (symmetric footprint, sum r_i = 0: every configured
 // one); a compile-time branch, so the common kernel carries only its mat-vec.
-template <int M, int TT, bool ELLK, bool BD>
+template <int M, int TT, bool ELLK, bool BD, bool FM>
 __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wpc = blockDim.x >> 5;
@@ -975,6 +1018,8 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
   for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
   for (int i = tid; i < ipc * (3 * QP + 2 * T_MAX); i += blockDim.x)
     (&wsbase[i / (3 * QP + 2 * T_MAX)].pxy[0].x)[i % (3 * QP + 2 * T_MAX)] = 0.f;
+  if (FM)
+    for (int i = tid; i < ipc * QP; i += blockDim.x) wsbase[i / QP].thsum[i % QP] = 0.0;
   BMC_STAMP(4);   // staging loops issued (thread 0)
   const bool all_circ = __syncthreads_and(circ);
   const bool all_cull = __syncthreads_and(cull);
@@ -1156,7 +1201,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
       team_sync(team, T);
       BMC_TICK(pc, 1);
       // ---- B: heading target --------------------------------------------------
-      phase_theta(Pt, Pt64, ws, lane, q, w, T);
+      phase_theta<FM>(Pt, Pt64, ws, lane, q, w, T, it >= 0);
       BMC_TICK(pc, 2);
       team_sync(team, T);
       BMC_TICK(pc, 3);
@@ -1167,13 +1212,19 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 #pragma unroll
       for (int ww = 0; ww < T_MAX; ++ww)
         if (ww < T) pth += ws->part_th[ww][k1];
+      if (FM && (k1 < 3 || k1 > 7)) pth = 0.0;   // not formed per iteration (see phase_theta)
       if (it >= 0) {
         if (k < NV) ws->rhspw[w][k] = lamp + rho_psi * pth;
         __syncwarp();
         {
           double s4[4] = {ub[2 * NV2 + k1], 0.0, 0.0, 0.0};
+          if (FM) {   // Kp11 vanishes outside rows / columns 3..7
 #pragma unroll
-          for (int j = 0; j < NV; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k1], ws->rhspw[w][j], s4[j & 3]);
+            for (int j = 3; j < 8; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k1], ws->rhspw[w][j], s4[j & 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) s4[j & 3] = fma(sf[BlobLayout::Kp11t + j * NV + k1], ws->rhspw[w][j], s4[j & 3]);
+          }
           const double v = (s4[0] + s4[1]) + (s4[2] + s4[3]);
           xi2r = (k < NV) ? v : 0.0;
           if (k < NV) {
@@ -1223,6 +1274,17 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     __syncwarp();
     BMC_STAMP(7);   // thread 0's team left the iteration loop
     if (lp_pending) lampsi_step();   // the last iteration's lambda_psi step
+    if constexpr (FM) {   // the boundary components' theta terms, contracted once
+      theta_sum_boundary(Pt64, ws, lane, q, w, T);
+      team_sync(team, T);
+      if (k < 3 || (k > 7 && k < NV)) {
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < T_MAX; ++ww)
+          if (ww < T) s += ws->part_th[ww][k];
+        lamp += rho_psi * s;
+      }
+    }
     // ---- outputs ----------------------------------------------------------------
     if (active) {
       float* co = a.coeffs + l * 5 * NV;
@@ -1300,7 +1362,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 size_t kernel_smem_bytes(int QPx, int n, int ipc, int team);
 
 // Launch of one (M, team size) kernel variant.
-template <int M, int TT, bool ELLK, bool BD>
+template <int M, int TT, bool ELLK, bool BD, bool FM>
 cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   // the shared-memory opt-in is per device: one bit per device ordinal (set on
   // the current device, which bmc_solve made params.device); racing threads
@@ -1310,28 +1372,36 @@ cudaError_t launch_am_mt(const KernelArgs& a, int ipc, cudaStream_t s) {
   if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
   const unsigned long long bit = 1ull << (dev & 63);
   if (dev >= 64 || !(attr_done.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT, ELLK, BD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(bmc_am_kernel<M, TT, ELLK, BD, FM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
 #ifdef BMC_PROFILE
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT, ELLK, BD>) == cudaSuccess)
+    if (cudaFuncGetAttributes(&fa, bmc_am_kernel<M, TT, ELLK, BD, FM>) == cudaSuccess)
       fprintf(stderr, "[bmc prof] kernel<%d,%d>: %d regs, max %d threads/block, %zu B local\n", M, TT, fa.numRegs,
               fa.maxThreadsPerBlock, fa.localSizeBytes);
 #endif
   }
   const size_t smem = smem_bytes(a.n, ipc, TT);
   const unsigned grid = (unsigned)((a.B + ipc - 1) / ipc);
-  bmc_am_kernel<M, TT, ELLK, BD><<<grid, 32 * TT * ipc, smem, s>>>(a);
+  bmc_am_kernel<M, TT, ELLK, BD, FM><<<grid, 32 * TT * ipc, smem, s>>>(a);
   return cudaGetLastError();
 }
 
+template <int M, int TT, bool FM>
+cudaError_t launch_am_f(const KernelArgs& a, int ipc, cudaStream_t s) {
+  if (a.blockdiag)
+    return a.alpha_rule ? launch_am_mt<M, TT, true, true, FM>(a, ipc, s) : launch_am_mt<M, TT, false, true, FM>(a, ipc, s);
+  return a.alpha_rule ? launch_am_mt<M, TT, true, false, FM>(a, ipc, s) : launch_am_mt<M, TT, false, false, FM>(a, ipc, s);
+}
+
+// FM (the full boundary set) for teams of 2 and 4: the per-sample theta sums need
+// shared memory that the one-warp-per-instance launches (large batches) do not have
 template <int M, int TT>
 cudaError_t launch_am_t(const KernelArgs& a, int ipc, cudaStream_t s) {
-  if (a.blockdiag)
-    return a.alpha_rule ? launch_am_mt<M, TT, true, true>(a, ipc, s) : launch_am_mt<M, TT, false, true>(a, ipc, s);
-  return a.alpha_rule ? launch_am_mt<M, TT, true, false>(a, ipc, s) : launch_am_mt<M, TT, false, false>(a, ipc, s);
+  if (TT >= 2 && a.nb == NB_MAX) return launch_am_f<M, TT, TT >= 2>(a, ipc, s);
+  return launch_am_f<M, TT, false>(a, ipc, s);
 }
 
 // One translation unit per circle count M (bmc_kernel_m<M>.cu) instantiates
