@@ -102,8 +102,9 @@ __device__ __forceinline__ void team_sync(int team, int T) {
 
 // u_x[22], u_y[22], u_psi[11] (+pad), then the per-lane weights of Dm and
 // Dm^T (DM_LO, DM_DI, DM_HI, DMT_LO, DMT_HI; [5][32], see dm_apply)
-constexpr int U_DOUBLES = 56 + 5 * 32;
+constexpr int U_DOUBLES = 56 + 5 * 32 + 16;
 constexpr int DM_TAB = 56;
+constexpr int CG_TAB = 56 + 5 * 32;   // FM: sum over the pinned j of (rho_psi P^T P)[k][j] u_psi[j], lanes k < 11
 
 // Development aid (make PROFILE=1): per-warp cycle counts of each phase.
 #ifdef BMC_PROFILE
@@ -1043,6 +1044,13 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     }
   }
   __syncthreads();
+  if (FM && tid < NV) {   // the pinned coefficients' part of (rho_psi P^T P) xi2 (xi2[j] = u_psi[j] there)
+    double s = 0.0;
+    for (int j = 0; j < NV; ++j)
+      if (j < 3 || j > 7) s = fma(sf[BlobLayout::Gppt + j * NV + tid], ub[2 * NV2 + j], s);
+    ub[CG_TAB + tid] = s;
+  }
+  __syncthreads();
   BMC_STAMP(1);   // prologue done
 
   Proj pa;
@@ -1111,8 +1119,14 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     auto lampsi_step = [&]() {
       const int k1 = min(k, NV - 1);
       double g4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (FM) {   // xi2 moves only in its coefficients 3..7
+        g4[0] = ub[CG_TAB + k1];
 #pragma unroll
-      for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
+        for (int j = 3; j < 8; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) g4[j & 3] = fma(sf[BlobLayout::Gppt + j * NV + k1], ws->xi2w[w][j], g4[j & 3]);
+      }
       const double v = lamp - (((g4[0] + g4[1]) + (g4[2] + g4[3])) - rho_psi * pth_prev);
       lamp = (k < NV) ? v : 0.0;
     };
