@@ -579,14 +579,18 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
     const unsigned bal = __ballot_sync(FULL, act);
     if (act) list[__popc(bal & ((1u << lane) - 1u))] = lane;
     na = __popc(bal);
-  } else {
+  } else {   // two words per step: both loads and ballots in flight
+    const unsigned below = (1u << lane) - 1u;
 #pragma unroll 1
-    for (int j0 = 0; j0 < npad; j0 += 32) {
-      const int j = j0 + lane;
-      const bool act = (j < npad) && !(clr[j] > lim);
-      const unsigned bal = __ballot_sync(FULL, act);
-      if (act) list[na + __popc(bal & ((1u << lane) - 1u))] = j;
-      na += __popc(bal);
+    for (int j0 = 0; j0 < npad; j0 += 64) {
+      const int ja = j0 + lane, jb = ja + 32;
+      const bool aa = (ja < npad) && !(clr[ja] > lim);
+      const bool ab = (jb < npad) && !(clr[jb] > lim);
+      const unsigned ba = __ballot_sync(FULL, aa), bb = __ballot_sync(FULL, ab);
+      const int nA = __popc(ba);
+      if (aa) list[na + __popc(ba & below)] = ja;
+      if (ab) list[na + nA + __popc(bb & below)] = jb;
+      na += nA + __popc(bb);
     }
   }
   __syncwarp();
