@@ -401,11 +401,13 @@ def test_error_codes():
         s.solve(_dev(pr["init"]), _dev(big), _dev(np.ones((161, 2), np.float32)), pr["bnd"], 3)
 
 
-@pytest.mark.parametrize("name,B", [("C1", 8), ("C3", 300), ("C4", 120)])
-def test_culling_is_exact(name, B, monkeypatch):
+@pytest.mark.parametrize("name,B,n", [("C1", 8, None), ("C3", 300, None), ("C4", 120, None), ("C3", 150, 100)])
+def test_culling_is_exact(name, B, n, monkeypatch):
     """The temporal culling of the inside test only skips obstacles whose contribution is
-    exactly zero: outputs are bitwise those of testing every obstacle (BMC_NOCULL=1)."""
-    cfg = CONFIGS[name]
+    exactly zero: outputs are bitwise those of testing every obstacle (BMC_NOCULL=1).
+    n = 100: the active list is built two 32-obstacle words at a time, the last step
+    with one partial word."""
+    cfg = CONFIGS[name] if n is None else CONFIGS[name].with_(n=n)
     pr = make_problem(cfg, 3, B=B)
     s = _solver(cfg)
     culled = run_gpu(cfg, pr, solver=s)
