@@ -31,7 +31,10 @@
  * Threading / streams: every function is re-entrant across contexts.  Calls
  * of bmc_solve on ONE context must be ordered on one stream (they share the
  * context's argmin workspace); bmc_solve_host has a workspace of its own and
- * may overlap them.  bmc_last_error() is thread-local.
+ * may overlap them, also from another thread (the context's host-side state is
+ * locked; host solves on one context run one at a time).  A constant blob
+ * uploaded on one stream is waited for (event) by solves on another.
+ * bmc_last_error() is thread-local.
  *
  * Determinism: an instance's outputs depend on its own inputs, the context and
  * the team size (warps per instance, bmc_problem.team) -- never on B, on its

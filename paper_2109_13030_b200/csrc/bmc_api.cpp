@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -55,7 +57,14 @@ struct Blob {
   int nb = 0;
   int blockdiag = 0;
   unsigned long long used = 0;  // LRU tick
+  cudaEvent_t ready = nullptr;  // recorded after the upload: solves on other streams wait for it
 };
+
+void free_blob(Blob& b) {
+  cudaFree(b.d);
+  if (b.h) cudaFreeHost(b.h);
+  if (b.ready) cudaEventDestroy(b.ready);
+}
 
 constexpr size_t BLOB_CACHE_MAX = 8;   // obstacle counts kept per context
 
@@ -83,7 +92,11 @@ struct bmc_ctx {
   unsigned int* ws_count_h = nullptr;
   cudaStream_t hstream = nullptr;
   HostBuf hb[10];
-  int32_t last_launches = 0;
+  std::atomic<int32_t> last_launches{0};
+  // host-side state shared by the entry points (blob cache, LRU tick): solves from
+  // several threads on one context serialise their launch sequences on `mu`;
+  // bmc_solve_host additionally holds `hmu` for its staging buffers and stream
+  std::mutex mu, hmu;
 };
 
 extern "C" {
@@ -92,7 +105,7 @@ int32_t bmc_version(void) { return 102; }
 
 const char* bmc_last_error(void) { return g_err.c_str(); }
 
-int32_t bmc_last_launch_count(const bmc_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+int32_t bmc_last_launch_count(const bmc_ctx* ctx) { return ctx ? ctx->last_launches.load() : 0; }
 
 int32_t bmc_sample_init(bmc_ctx* ctx, const bmc_sample_params* sp, float* init, bmc_stream_t stream) {
   if (!ctx) return fail(BMC_EINVAL, "ctx is NULL");
@@ -217,10 +230,7 @@ int32_t bmc_setup(const bmc_params* params, bmc_ctx** out) {
 void bmc_destroy(bmc_ctx* c) {
   if (!c) return;
   DeviceGuard g(c->p.device);
-  for (auto& kv : c->blobs) {
-    cudaFree(kv.second.d);
-    if (kv.second.h) cudaFreeHost(kv.second.h);
-  }
+  for (auto& kv : c->blobs) free_blob(kv.second);
   if (c->ws_key) cudaFree(c->ws_key);
   for (auto& b : c->hb) cudaFree(b.p);
   if (c->hstream) cudaStreamDestroy(c->hstream);
@@ -249,8 +259,7 @@ static int32_t get_blob(bmc_ctx* c, int n, cudaStream_t stream, Blob** out) {
     for (auto jt = c->blobs.begin(); jt != c->blobs.end(); ++jt)
       if (jt->second.used < lru->second.used) lru = jt;
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize(blob eviction)");
-    cudaFree(lru->second.d);
-    cudaFreeHost(lru->second.h);
+    free_blob(lru->second);
     c->blobs.erase(lru);
   }
   Blob b;
@@ -267,9 +276,14 @@ static int32_t get_blob(bmc_ctx* c, int n, cudaStream_t stream, Blob** out) {
     cudaFreeHost(b.h);
     return cuda_fail(e, "cudaMalloc(blob)");
   }
-  if ((e = cudaMemcpyAsync(b.d, b.h, bytes, cudaMemcpyHostToDevice, stream)) != cudaSuccess) {
-    cudaFree(b.d);
-    cudaFreeHost(b.h);
+  if ((e = cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming)) != cudaSuccess) {
+    b.ready = nullptr;
+    free_blob(b);
+    return cuda_fail(e, "cudaEventCreate(blob)");
+  }
+  if ((e = cudaMemcpyAsync(b.d, b.h, bytes, cudaMemcpyHostToDevice, stream)) != cudaSuccess ||
+      (e = cudaEventRecord(b.ready, stream)) != cudaSuccess) {
+    free_blob(b);
     return cuda_fail(e, "cudaMemcpyAsync(blob)");
   }
   c->blobs[n] = b;
@@ -348,9 +362,13 @@ int32_t bmc_team_for(const bmc_ctx* c, int64_t B) {
 
 static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* rs, cudaStream_t s,
                           unsigned long long* ws_key, unsigned int* ws_count) {
+  std::lock_guard<std::mutex> lock(c->mu);
   Blob* blob = nullptr;
   int32_t rc = get_blob(c, pr->n_obs, s, &blob);
   if (rc != BMC_OK) return rc;
+  // the upload may have been issued on another stream (bmc_solve vs bmc_solve_host)
+  cudaError_t ew = cudaStreamWaitEvent(s, blob->ready, 0);
+  if (ew != cudaSuccess) return cuda_fail(ew, "cudaStreamWaitEvent(blob)");
   int ipc = 1, team = 1;
   launch_shape(c, pr->B, pr->team, &ipc, &team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024) --ipc;
@@ -533,6 +551,7 @@ static int32_t ensure(bmc_ctx* c, int slot, size_t bytes, void** out) {
 int32_t bmc_solve_host(bmc_ctx* c, const bmc_problem* ph, const bmc_result* rh) {
   int32_t rc = validate_problem(c, ph, rh);
   if (rc != BMC_OK) return rc;
+  std::lock_guard<std::mutex> hlock(c->hmu);
   DeviceGuard g(c->p.device);
   c->last_launches = 0;
   cudaError_t e;

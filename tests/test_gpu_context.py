@@ -44,3 +44,46 @@ def test_constant_cache_eviction_and_async_upload():
         ref = _solve(solver_for(cfg, device=0), cfg, pr)
         for k in ("coeffs", "lambda_out", "residual", "cost", "best"):
             assert np.array_equal(got[k], ref[k]), (n, k)
+
+
+def test_host_and_device_solves_from_two_threads():
+    """bmc_solve (one thread, its own stream) and bmc_solve_host (another thread) on ONE
+    context at the same time, with obstacle counts first seen by either path (so a blob
+    uploaded on one stream is used by the other): every result is bitwise that of a
+    fresh context solving alone (include/bmc.h "Threading / streams")."""
+    import threading
+    from paper_2109_13030_b200 import solver_for
+    base = CONFIGS["C2"].with_(B=37, K=20)
+    cases = {n: (base.with_(n=n), make_problem(base.with_(n=n), 50 + n)) for n in (5, 7, 9, 13)}
+    ref = {n: _solve(solver_for(cfg, device=0), cfg, pr) for n, (cfg, pr) in cases.items()}
+    shared = solver_for(base.with_(n=5), device=0)
+    errors, got_dev, got_host = [], [], []
+
+    def device_loop():
+        try:
+            st = torch.cuda.Stream()
+            for n in (7, 5, 13, 7, 9, 5):
+                cfg, pr = cases[n]
+                with torch.cuda.stream(st):
+                    got_dev.append((n, _solve(shared, cfg, pr, stream=st)))
+        except Exception as e:   # pragma: no cover - reported below
+            errors.append(e)
+
+    def host_loop():
+        try:
+            for n in (9, 13, 5, 7, 9, 13):
+                cfg, pr = cases[n]
+                got_host.append((n, shared.solve_host(pr["init"], pr["obs_xy"], pr["obs_ab"], pr["bnd"], cfg.K)))
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=device_loop), threading.Thread(target=host_loop)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    assert len(got_dev) == 6 and len(got_host) == 6
+    for n, g in got_dev + got_host:
+        for k in ("coeffs", "lambda_out", "residual", "cost", "best"):
+            assert np.array_equal(g[k], ref[n][k]), (n, k)
