@@ -10,6 +10,8 @@ the iteration count (0..40), the batch (1..300), the team size (0 = automatic, 1
 2, 4) and a warm or cold start.  A mask that leaves the KKT singular must be
 refused by both sides (BMC_ESINGULAR / the oracle's error).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -56,7 +58,11 @@ def _case(seed):
     return cfg, kw, ellipses, team, warm, rng
 
 
-@pytest.mark.parametrize("seed", range(64))
+# BMC_FUZZ_SEEDS=a:b widens the sweep for a one-off run (default: seeds 0..63)
+_SEEDS = range(*map(int, os.environ.get("BMC_FUZZ_SEEDS", "0:64").split(":")))
+
+
+@pytest.mark.parametrize("seed", _SEEDS)
 def test_random_configuration(seed):
     from paper_2109_13030_b200 import BmcError, solver_for
     cfg, kw, ellipses, team, warm, rng = _case(seed)
