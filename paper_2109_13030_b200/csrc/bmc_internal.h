@@ -39,9 +39,11 @@ struct BlobLayout {
   static constexpr int n_doubles_raw = Gdd + NV * NV;
   static constexpr int n_doubles = (n_doubles_raw + 1) & ~1;   // 16-byte multiple
   static constexpr size_t bytes_f64 = sizeof(double) * n_doubles;
-  // fp32 section: Pt[11][QP] = P transposed, zero for t >= q (Pdot = P Dm and
+  // fp32 section: Pt[QP][PT_ROW] = the basis row of sample t (11 values + a zero
+  // pad: three 16-byte loads per sample), zero for t >= q (Pdot = P Dm and
   // Pddot = P Dm^2 are applied on the coefficient side, bmc_kernel.cuh dm_apply)
-  BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * NV * (size_t)QP; }
+  static constexpr int PT_ROW = 12;
+  BMC_HD static size_t bytes_f32(int QP) { return sizeof(float) * PT_ROW * (size_t)QP; }
   // fp64 copy of the same basis for the F^T (F xi - g) and P^T theta contractions,
   // row stride QP + 4 doubles: the 8 rows of an FP64 MMA A-fragment then fall
   // on distinct shared-memory banks

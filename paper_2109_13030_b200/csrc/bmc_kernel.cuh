@@ -398,9 +398,14 @@ __device__ __forceinline__ void load12(const float* src, float (&c)[NV]) {
   c[8] = d.x; c[9] = d.y; c[10] = d.z;
 }
 
+// the fp32 basis row of sample t (BlobLayout: [QP][12], three 16-byte loads)
+__device__ __forceinline__ void load_basis_row(const float* Pt, int t, float (&p)[NV]) {
+  load12(Pt + t * BlobLayout::PT_ROW, p);
+}
+
 // Per-kernel constants of the projection phase (registers / constant bank).
 struct Proj {
-  const float* Pt;       // smem basis [3][11][QP]
+  const float* Pt;       // smem basis [QP][12] (fp32, per-sample rows)
   const double* Pt64;    // the same basis in fp64 (contractions)
   const float2* obs;     // smem obstacles [n][QP], relative to the boundary line
   const float4* abi;     // smem (a, b, a b, kind) per obstacle
@@ -537,10 +542,16 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
       const float x2 = xt * xt, y2 = yt * yt;
       float dx, dy;
       if (ab.w == 1.f) {
+        // f = N / D >= 1 / rho (d* >= 1): a f - 1 = b (a - b) y~^2 / D and
+        // b f - 1 = a (b - a) x~^2 / D exactly, formed without the cancellation of
+        // a f - 1 (a far obstacle leaves a f ~ 1, and fp32 would keep only the
+        // rounding error of a f); otherwise f = 1 / rho (inside, d = 1)
         const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
-        const float f = fmaxf(rsqrt_ftz(x2 + y2), __fdividef(N, D));
-        dx = xt * fmaf(a, f, -1.f);
-        dy = yt * fmaf(b, f, -1.f);
+        const float ri = rsqrt_ftz(x2 + y2), rD = __frcp_rn(D);
+        const bool out = N * rD >= ri;
+        const float amb = a - b;   // exact (Sterbenz) for b <= a <= 2 b and vice versa
+        dx = out ? xt * ((b * amb) * y2 * rD) : xt * fmaf(a, ri, -1.f);
+        dy = out ? yt * ((-a * amb) * x2 * rD) : yt * fmaf(b, ri, -1.f);
       } else {
         const float R2 = (ab.w == 0.f) ? x2 + y2 : fmaf(a * a, y2, b * b * x2);
         const float num = (ab.w == 0.f) ? a : ab.z;
@@ -624,8 +635,7 @@ __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const 
     if (u >= nr) break;
     const int t = 32 * u + lane;
     float p[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) p[k] = Pt[k * QP + t];
+    load_basis_row(Pt, t, p);
     float2 cs = make_float2(0.f, 0.f);   // (c, s) = (P c_c, P c_s)
 #pragma unroll
     for (int k = 0; k < NV; ++k) cs = fma2(bc2(p[k]), ccs[k], cs);
@@ -744,11 +754,12 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
     float2 xy = make_float2(0.f, 0.f), xyd = xy, xydd = xy;
     float psi = 0.f;
     {
-      float cp[NV];
+      float cp[NV], pr[NV];
       load12(ws->cf4[w], cp);
+      load_basis_row(Pt, t, pr);
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
-        const float p = Pt[k * QP + t];
+        const float p = pr[k];
         const float4 c0 = *reinterpret_cast<const float4*>(&ws->cfi[k][0]);
         const float2 c1 = *reinterpret_cast<const float2*>(&ws->cfi[k][4]);
         xy = fma2(bc2(p), make_float2(c0.x, c0.y), xy);

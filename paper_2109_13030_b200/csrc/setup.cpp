@@ -232,13 +232,14 @@ int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err)
   delete[] out->pt;
   delete[] out->pt64;
   const int S64 = BlobLayout::p64_stride(QP);
-  out->pt = new float[NV * QP];
+  constexpr int PR = BlobLayout::PT_ROW;
+  out->pt = new float[PR * QP];
   out->pt64 = new double[NV * S64];
-  std::memset(out->pt, 0, sizeof(float) * NV * QP);
+  std::memset(out->pt, 0, sizeof(float) * PR * QP);
   std::memset(out->pt64, 0, sizeof(double) * NV * S64);
   for (int k = 0; k < NV; ++k)
     for (int t = 0; t < q; ++t) {
-      out->pt[k * QP + t] = (float)P[t * NV + k];
+      out->pt[t * PR + k] = (float)P[t * NV + k];
       out->pt64[k * S64 + t] = P[t * NV + k];
     }
   // The kernel evaluates Pdot c as P (Dm c) and Pdot^T u as Dm^T (P^T u) with the
