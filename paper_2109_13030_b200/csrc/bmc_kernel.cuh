@@ -67,9 +67,11 @@ struct alignas(16) WarpSmemT {
   double xi2w[TT][12];    // per-warp copies of xi2 (the heading step is redundant)
   double rhspw[TT][12];
   // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
-  // c_y - c_ref_y, Dm c_x, Dm c_y, Dm^2 c_x, Dm^2 c_y, c_c, c_s (Dm: the
-  // derivative operator on coefficients, Pdot = P Dm)
-  float cfi[NV + 1][8];
+  // c_y - c_ref_y, Dm c_x, Dm c_y, Dm^2 c_x, Dm^2 c_y (Dm: the derivative
+  // operator on coefficients, Pdot = P Dm), 2 pad; the
+  // copies (c_c, c_s) per k, two indices per 16-byte load
+  alignas(16) float cpos[NV + 1][8];
+  alignas(16) float ccs[NV + 1][2];
   float cf4[TT][12];      // per-warp fp32 c_psi
   float2 cs[QP];                // copies (c, s) per sample
   float th[QP];                 // theta per sample
@@ -621,9 +623,13 @@ __device__ __forceinline__ int build_active(const float* __restrict__ clr, int* 
 template <bool FM, class WarpSmem>
 __device__ __forceinline__ void phase_theta(const float* __restrict__ Pt, const double* __restrict__ Pt64,
                                             WarpSmem* ws, int lane, int q, int w, int T, bool sum_theta) {
-  float2 ccs[NV];   // (c_c, c_s) per Bernstein index
+  float2 ccs[NV + 1];   // (c_c, c_s) per Bernstein index
 #pragma unroll
-  for (int k = 0; k < NV; ++k) ccs[k] = *reinterpret_cast<const float2*>(&ws->cfi[k][6]);
+  for (int k = 0; k < NV + 1; k += 2) {
+    const float4 v = reinterpret_cast<const float4*>(&ws->ccs[0][0])[k >> 1];
+    ccs[k] = make_float2(v.x, v.y);
+    ccs[k + 1] = make_float2(v.z, v.w);
+  }
   constexpr int NA = FM ? 5 : 16;
   double acc[NA];   // P^T theta in fp64 (exact products, no cancellation loss)
 #pragma unroll
@@ -760,8 +766,8 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const float p = pr[k];
-        const float4 c0 = *reinterpret_cast<const float4*>(&ws->cfi[k][0]);
-        const float2 c1 = *reinterpret_cast<const float2*>(&ws->cfi[k][4]);
+        const float4 c0 = *reinterpret_cast<const float4*>(&ws->cpos[k][0]);
+        const float2 c1 = *reinterpret_cast<const float2*>(&ws->cpos[k][4]);
         xy = fma2(bc2(p), make_float2(c0.x, c0.y), xy);
         xyd = fma2(bc2(p), make_float2(c0.z, c0.w), xyd);
         xydd = fma2(bc2(p), c1, xydd);
@@ -1028,7 +1034,9 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     cull &= (kind != 1.f);   // the literal rule has no zero offset outside the ellipse (G8)
   }
   for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
-    (&wsbase[i / ((NV + 1) * 8)].cfi[0][0])[i % ((NV + 1) * 8)] = 0.f;
+    (&wsbase[i / ((NV + 1) * 8)].cpos[0][0])[i % ((NV + 1) * 8)] = 0.f;
+  for (int i = tid; i < ipc * (NV + 1) * 2; i += blockDim.x)
+    (&wsbase[i / ((NV + 1) * 2)].ccs[0][0])[i % ((NV + 1) * 2)] = 0.f;
   for (int i = tid; i < ipc * TT * 12; i += blockDim.x)
     (&wsbase[i / (TT * 12)].cf4[0][0])[i % (TT * 12)] = 0.f;
   for (int i = tid; i < ipc * 8 * QPU; i += blockDim.x) (&wsbase[i / (8 * QPU)].U[0][0])[i % (8 * QPU)] = 0.f;
@@ -1216,11 +1224,11 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           const int kp = min(k, NV - 1), kq = min(max(k - NV, 0), NV - 1);
           const float xf = d2f(xi[c] - cref[c]), d1f = d2f(d1), d2ff = d2f(d2), cf = d2f(xi[c]);
           if (k < NV) {
-            ws->cfi[kp][ch] = xf;
-            ws->cfi[kp][2 + ch] = d1f;
-            ws->cfi[kp][4 + ch] = d2ff;
+            ws->cpos[kp][ch] = xf;
+            ws->cpos[kp][2 + ch] = d1f;
+            ws->cpos[kp][4 + ch] = d2ff;
           }
-          if (k >= NV && k < NV2) ws->cfi[kq][6 + ch] = cf;
+          if (k >= NV && k < NV2) ws->ccs[kq][ch] = cf;
         }
         if (k < NV2) ws->xi1[ch][k] = xi[c];
       }
