@@ -36,7 +36,13 @@ struct BlobLayout {
   static constexpr int Kp12t = Kp11t + NV * NV;      // [6][11]
   static constexpr int Gppt = Kp12t + NB_MAX * NV;   // [11][11] rho_psi P^T P
   static constexpr int Gdd = Gppt + NV * NV;         // [11][11] Pdd^T Pdd (cost)
-  static constexpr int n_doubles_raw = Gdd + NV * NV;
+  // block-diagonal M and K11 (sum r_i = 0), row-major: row k holds the 11 entries
+  // of its own block (columns j0 .. j0 + 10, j0 = 0 or 11) and 3 zeros; the
+  // 112-byte stride keeps each quarter-warp of a 16-byte load on distinct banks
+  static constexpr int BD_ROW = 14;
+  static constexpr int Mb = (Gdd + NV * NV + 1) & ~1;     // [22][BD_ROW]
+  static constexpr int Kb = Mb + NV2 * BD_ROW;            // [22][BD_ROW]
+  static constexpr int n_doubles_raw = Kb + NV2 * BD_ROW;
   static constexpr int n_doubles = (n_doubles_raw + 1) & ~1;   // 16-byte multiple
   static constexpr size_t bytes_f64 = sizeof(double) * n_doubles;
   // fp32 section: Pt[QP][PT_ROW] = the basis row of sample t (11 values + a zero

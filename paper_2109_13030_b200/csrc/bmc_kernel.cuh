@@ -60,10 +60,15 @@ constexpr int HP_SLOTS = 8 * 12; // per-warp partial contractions (D2), doubles
 // the lambda step (Eq. 10: F and the KKT are block diagonal over channels), so a
 // team gives each channel to one warp; the small heading step runs redundantly
 // in every warp.
+// slot of coefficient k (0..21) in WarpSmem::xi1 / rhs
+__host__ __device__ constexpr int xpad(int k) { return k + (k >= NV ? 1 : 0); }
+
 template <int TT>
 struct alignas(16) WarpSmemT {
-  double xi1[2][24];      // [ch][k] current xi1 (fp64), written by the channel's owner
-  double rhs[2][24];      // [ch][k] lambda - rho h
+  // [ch][xpad(k)] current xi1 (fp64), written by the channel's owner; the copy
+  // block starts at 12 (16-byte aligned pairs for the block-diagonal step)
+  double xi1[2][24];
+  double rhs[2][24];      // [ch][xpad(k)] lambda - rho h
   double xi2w[TT][12];    // per-warp copies of xi2 (the heading step is redundant)
   double rhspw[TT][12];
   // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
@@ -1174,7 +1179,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c >= nown) break;
-          if (k < NV2) ws->rhs[chb + c][k] = lam[c] - rho * hreg[c];
+          if (k < NV2) ws->rhs[chb + c][xpad(k)] = lam[c] - rho * hreg[c];
         }
         __syncwarp();
         if (nown > 0 && lp_pending) lampsi_step();
@@ -1188,19 +1193,27 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           // symmetric footprint M and K11 are block diagonal (setup.cpp): row k only
           // meets the columns of its own block (c_x rows 0..10, c_c rows 11..21).
           double acc[8] = {ub[ch * NV2 + kc], 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-          if (BD) {
-            const int j0 = (kc < NV) ? 0 : NV;
+          if (BD) {   // row kc of its block and the block's vector entries, two per 16-byte load
+            const int j0 = (kc < NV) ? 0 : xpad(NV);
+            const double2* mrow = reinterpret_cast<const double2*>(sf + BlobLayout::Mb + kc * BlobLayout::BD_ROW);
+            const double2* krow = reinterpret_cast<const double2*>(sf + BlobLayout::Kb + kc * BlobLayout::BD_ROW);
+            const double2* xv = reinterpret_cast<const double2*>(&ws->xi1[ch][j0]);
+            const double2* rv = reinterpret_cast<const double2*>(&ws->rhs[ch][j0]);
 #pragma unroll
-            for (int jj = 0; jj < NV; ++jj) {
-              const int j = j0 + jj;
-              acc[jj & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[jj & 3]);
-              acc[4 + (jj & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (jj & 3)]);
+            for (int jj = 0; jj < NV; jj += 2) {
+              const double2 m2 = mrow[jj >> 1], k2 = krow[jj >> 1], x2 = xv[jj >> 1], r2 = rv[jj >> 1];
+              acc[jj & 3] = fma(m2.x, x2.x, acc[jj & 3]);
+              acc[4 + (jj & 3)] = fma(k2.x, r2.x, acc[4 + (jj & 3)]);
+              if (jj + 1 < NV) {
+                acc[(jj + 1) & 3] = fma(m2.y, x2.y, acc[(jj + 1) & 3]);
+                acc[4 + ((jj + 1) & 3)] = fma(k2.y, r2.y, acc[4 + ((jj + 1) & 3)]);
+              }
             }
           } else {
 #pragma unroll
             for (int j = 0; j < NV2; ++j) {
-              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][j], acc[j & 3]);
-              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][j], acc[4 + (j & 3)]);
+              acc[j & 3] = fma(sf[BlobLayout::Mt + j * NV2 + kc], ws->xi1[ch][xpad(j)], acc[j & 3]);
+              acc[4 + (j & 3)] = fma(sf[BlobLayout::K11t + j * NV2 + kc], ws->rhs[ch][xpad(j)], acc[4 + (j & 3)]);
             }
           }
           const double v = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
@@ -1230,7 +1243,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           }
           if (k >= NV && k < NV2) ws->ccs[kq][ch] = cf;
         }
-        if (k < NV2) ws->xi1[ch][k] = xi[c];
+        if (k < NV2) ws->xi1[ch][xpad(k)] = xi[c];
       }
       if (nown == 0 && lp_pending) lampsi_step();   // warps without a channel (T = 4)
       lp_pending = false;

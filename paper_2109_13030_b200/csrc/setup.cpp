@@ -218,6 +218,11 @@ int build_consts(const SetupParams& p, int n, HostConsts* out, std::string* err)
       const bool off = out->blockdiag && ((k < NV) != (j < NV));
       f[BlobLayout::Mt + j * NV2 + k] = off ? 0.0 : p.rho * mkj;
       f[BlobLayout::K11t + j * NV2 + k] = off ? 0.0 : Ki[k * N1 + j];
+      if (out->blockdiag && !off) {   // row-major copy of the own block
+        const int jj = j - (k < NV ? 0 : NV);
+        f[BlobLayout::Mb + k * BlobLayout::BD_ROW + jj] = p.rho * mkj;
+        f[BlobLayout::Kb + k * BlobLayout::BD_ROW + jj] = Ki[k * N1 + j];
+      }
     }
   for (int rr = 0; rr < nb; ++rr)
     for (int k = 0; k < NV2; ++k) f[BlobLayout::K12t + rr * NV2 + k] = Ki[k * N1 + NV2 + rr];
