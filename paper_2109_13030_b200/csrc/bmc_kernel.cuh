@@ -73,9 +73,10 @@ struct alignas(16) WarpSmemT {
   double rhspw[TT][12];
   // fp32 coefficients interleaved per Bernstein index k: c_x - c_ref_x,
   // c_y - c_ref_y, Dm c_x, Dm c_y, Dm^2 c_x, Dm^2 c_y (Dm: the derivative
-  // operator on coefficients, Pdot = P Dm), 2 pad; the
-  // copies (c_c, c_s) per k, two indices per 16-byte load
-  alignas(16) float cpos[NV + 1][8];
+  // operator on coefficients, Pdot = P Dm); the copies
+  // (c_c, c_s) per k, two indices per 16-byte load
+  alignas(16) float cpos[NV + 1][4];   // (c_x - c_ref_x, c_y - c_ref_y, Dm c_x, Dm c_y)
+  alignas(16) float cdd[NV + 1][2];    // (Dm^2 c_x, Dm^2 c_y), two indices per 16-byte load
   alignas(16) float ccs[NV + 1][2];
   float cf4[TT][12];      // per-warp fp32 c_psi
   float2 cs[QP];                // copies (c, s) per sample
@@ -772,10 +773,11 @@ __device__ __forceinline__ void phase_project(const Proj& pa, const float (&r)[M
       for (int k = 0; k < NV; ++k) {
         const float p = pr[k];
         const float4 c0 = *reinterpret_cast<const float4*>(&ws->cpos[k][0]);
-        const float2 c1 = *reinterpret_cast<const float2*>(&ws->cpos[k][4]);
+        float4 c1;   // Dm^2 c of indices k, k + 1
+        if (!(k & 1)) c1 = reinterpret_cast<const float4*>(&ws->cdd[0][0])[k >> 1];
         xy = fma2(bc2(p), make_float2(c0.x, c0.y), xy);
         xyd = fma2(bc2(p), make_float2(c0.z, c0.w), xyd);
-        xydd = fma2(bc2(p), c1, xydd);
+        xydd = fma2(bc2(p), (k & 1) ? make_float2(c1.z, c1.w) : make_float2(c1.x, c1.y), xydd);
         psi = fmaf(p, cp[k], psi);
       }
     }
@@ -1038,8 +1040,10 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
     circ &= (aa == bb);
     cull &= (kind != 1.f);   // the literal rule has no zero offset outside the ellipse (G8)
   }
-  for (int i = tid; i < ipc * (NV + 1) * 8; i += blockDim.x)
-    (&wsbase[i / ((NV + 1) * 8)].cpos[0][0])[i % ((NV + 1) * 8)] = 0.f;
+  for (int i = tid; i < ipc * (NV + 1) * 4; i += blockDim.x)
+    (&wsbase[i / ((NV + 1) * 4)].cpos[0][0])[i % ((NV + 1) * 4)] = 0.f;
+  for (int i = tid; i < ipc * (NV + 1) * 2; i += blockDim.x)
+    (&wsbase[i / ((NV + 1) * 2)].cdd[0][0])[i % ((NV + 1) * 2)] = 0.f;
   for (int i = tid; i < ipc * (NV + 1) * 2; i += blockDim.x)
     (&wsbase[i / ((NV + 1) * 2)].ccs[0][0])[i % ((NV + 1) * 2)] = 0.f;
   for (int i = tid; i < ipc * TT * 12; i += blockDim.x)
@@ -1239,7 +1243,7 @@ __global__ void BMC_KERNEL_BOUNDS bmc_am_kernel(const __grid_constant__ KernelAr
           if (k < NV) {
             ws->cpos[kp][ch] = xf;
             ws->cpos[kp][2 + ch] = d1f;
-            ws->cpos[kp][4 + ch] = d2ff;
+            ws->cdd[kp][ch] = d2ff;
           }
           if (k >= NV && k < NV2) ws->ccs[kq][ch] = cf;
         }
