@@ -491,7 +491,8 @@ static void heading_target(const or_ctx* c, const traj_t* tr) {
  * F^T of the residual rows, lambda, J) stays fp64 as it is there.  Sites:
  *   evaluation: coefficients (positions relative to the boundary line, the
  *     frame the product path keeps positions in), the fp32 basis, and every
- *     evaluated sample x, y, xdot, ydot, xddot, yddot, psi, c, s;
+ *     evaluated sample x, y, xdot, ydot, xddot, yddot, psi, c, s (x, y, psi,
+ *     c, s: every partial sum of the k-ordered FMA chain, eval32);
  *   cos psi, sin psi, theta = atan2(s, c);
  *   obstacle positions relative to the boundary line (once, to nearest);
  *   circle centres, (x~, y~), and every projection offset delta = g - v;
@@ -533,12 +534,15 @@ static double r32(const r32_t* z, int site, long long idx, double v) {
   return u < p ? (double)hi : (double)lo;
 }
 
-/* sum_k B[t][k] coef_k rounded (the coefficients rounded first) */
+/* sum_k B[t][k] coef_k as the product path forms it (the coefficients rounded
+ * first): a chain of fused multiply-adds in k order, every partial sum held in
+ * fp32 and so rounded where it is formed (the product of two fp32 values is exact
+ * in fp64, so r32(s + B coef) is one fp32 FMA) */
 static double eval32(const r32_t* z, int site, const double* B, int t, const double* coef) {
   const int nv = z->c->nv;
   double s = 0.0;
-  for (int k = 0; k < nv; ++k) s += B[t * nv + k] * coef[k];
-  return r32(z, site, t, s);
+  for (int k = 0; k < nv; ++k) s = r32(z, site, (long long)t * 16 + k, s + B[t * nv + k] * coef[k]);
+  return s;
 }
 
 /* theta from the fp32 copies (model counterpart of heading_target) */

@@ -44,3 +44,8 @@ except AssertionError as e:
     print("FAIL", msg[msg.find("'max_dtraj'"):msg.find("'fp32_model_accepted'")], msg[msg.find("failing instances"):])
 J = np.asarray(r["cost"]); dJ = np.abs(g["cost"] - J) / np.abs(J)
 print("rel dJ: median %.2e p90 %.2e max %.2e" % (np.median(dJ), np.percentile(dJ, 90), dJ.max()))
+lg = np.asarray(g["lambda_out"], np.float64).reshape(len(J), -1); lr = np.asarray(r["lambda_out"]).reshape(len(J), -1)
+dl = np.abs(lg - lr).max(1); worst = int(dl.argmax())
+print("lambda: worst inst %d dlam %.2e max|lam| %.2e; worst entry %d (channel block %d)" %
+      (worst, dl[worst], np.abs(lr[worst]).max(), int(np.abs(lg[worst] - lr[worst]).argmax()),
+       int(np.abs(lg[worst] - lr[worst]).argmax()) // 11))
