@@ -555,11 +555,14 @@ __device__ __forceinline__ void coll_general(const bool RES, const bool GUARD, c
         // a f - 1 (a far obstacle leaves a f ~ 1, and fp32 would keep only the
         // rounding error of a f); otherwise f = 1 / rho (inside, d = 1)
         const float N = fmaf(b, y2, a * x2), D = fmaf(b * b, y2, a * a * x2);
-        const float ri = rsqrt_ftz(x2 + y2), rD = __frcp_rn(D);
+        const float ri = rsqrt_ftz(x2 + y2), rD = rcp_approx(D);   // ~1 ulp, no cancellation after it
         const bool out = N * rD >= ri;
         const float amb = a - b;   // exact (Sterbenz) for b <= a <= 2 b and vice versa
-        dx = out ? xt * ((b * amb) * y2 * rD) : xt * fmaf(a, ri, -1.f);
-        dy = out ? yt * ((-a * amb) * x2 * rD) : yt * fmaf(b, ri, -1.f);
+        const float kx = b * amb, ky = -a * amb;   // per obstacle
+        const float fx = out ? kx * y2 * rD : fmaf(a, ri, -1.f);
+        const float fy = out ? ky * x2 * rD : fmaf(b, ri, -1.f);
+        dx = xt * fx;
+        dy = yt * fy;
       } else {
         const float R2 = (ab.w == 0.f) ? x2 + y2 : fmaf(a * a, y2, b * b * x2);
         const float num = (ab.w == 0.f) ? a : ab.z;
