@@ -14,7 +14,7 @@ r=np.array(cfg.offsets); rabs=np.abs(r).max()
 ox=pr["obs_xy"][:,0,:].astype(np.float64); oy=pr["obs_xy"][:,1,:].astype(np.float64); a=pr["obs_ab"][:,0].astype(np.float64)
 QP=128; margin=2e-3
 rng=np.random.default_rng(0)
-def sim(G, insts):
+def sim(G, insts, coef=False):
     tests=0; its=0
     for l in insts:
         tr=o.trace_instance(pr["bnd"], pr["obs_xy"], pr["obs_ab"], pr["init"][l], cfg.K)
@@ -27,7 +27,15 @@ def sim(G, insts):
             x=np.zeros(QP); y=np.zeros(QP); ps=np.zeros(QP)
             x[:cfg.q]=P@cx; y[:cfg.q]=P@cy; ps[:cfg.q]=P@cp
             mv=np.hypot(x-px, y-py)+rabs*np.abs(ps-pp); px,py,pp=x,y,ps
-            A+=mv.reshape(ngr,G).max(1)
+            if coef:   # one clock per instance from the coefficient changes (convex hull bound)
+                if k == 0:
+                    A += mv.reshape(ngr, G).max(1)
+                else:
+                    dcx = np.abs(cx - pcx).max(); dcy = np.abs(cy - pcy).max(); dcp = np.abs(cp - pcp).max()
+                    A += np.hypot(dcx, dcy) + rabs * dcp
+                pcx, pcy, pcp = cx.copy(), cy.copy(), cp.copy()
+            else:
+                A+=mv.reshape(ngr,G).max(1)
             # circle centres and clearance per (sample, obstacle)
             X=x[:cfg.q,None]+r[None,:]*np.cos(ps[:cfg.q,None]); Y=y[:cfg.q,None]+r[None,:]*np.sin(ps[:cfg.q,None])
             d=np.sqrt((X[:,:,None]-ox.T[:,None,:])**2+(Y[:,:,None]-oy.T[:,None,:])**2).min(1)-a[None,:]  # q x n
@@ -45,3 +53,4 @@ def sim(G, insts):
 insts=rng.choice(cfg.B, 24, replace=False)
 for G in (32,16,8,4):
     print("group", G, "tested (round, obstacle) per instance-iteration", round(sim(G, insts),2))
+print("coefficient clock (one per instance), rounds of 32:", round(sim(32, insts, coef=True), 2))
