@@ -127,3 +127,43 @@ def test_sincos_fast_accuracy():
     es, ec = s - np.sin(xs), c - np.cos(xs)
     assert np.abs(es).max() < 1.5e-7 and np.abs(ec).max() < 1.5e-7
     assert abs(es.mean()) < 1e-9 and abs(ec.mean()) < 1e-9
+
+
+def test_literal_rule_offset_without_cancellation():
+    """Literal-rule ellipse offset (Eq. 21a/22a with alpha = atan2(y~, x~), G8): outside
+    (d* >= 1) the kernel forms a f - 1 and b f - 1 (f = N / D) as b (a - b) y~^2 / D and
+    a (b - a) x~^2 / D.  Check the identity against the paper's form in fp64, and that in
+    fp32 the rewritten form keeps ~1e-7 relative accuracy on nearly circular ellipses,
+    where a f - 1 is a small difference of O(1) values and the direct form keeps only
+    its rounding error (bmc_kernel.cuh coll_general)."""
+    rng = np.random.default_rng(7)
+    # the kernel's inputs are fp32 (obs_ab, x~, y~): draw them as fp32 values
+    a = rng.uniform(0.4, 0.9, 2000).astype(np.float32).astype(np.float64)
+    b = (a * (1.0 - rng.uniform(1e-3, 1e-2, 2000))).astype(np.float32).astype(np.float64)   # nearly circular
+    ang = rng.uniform(-np.pi, np.pi, 2000)
+    rho = rng.uniform(2.0, 40.0, 2000)       # outside every ellipse
+    xt = (rho * np.cos(ang)).astype(np.float32).astype(np.float64)
+    yt = (rho * np.sin(ang)).astype(np.float32).astype(np.float64)
+    # the paper's form: delta = (a d cos(al) - x~, b d sin(al) - y~), d = max(1, d*)
+    al = np.arctan2(yt, xt)
+    dstar = (a * xt * np.cos(al) + b * yt * np.sin(al)) / (a**2 * np.cos(al)**2 + b**2 * np.sin(al)**2)
+    d = np.maximum(dstar, 1.0)
+    dx_ref, dy_ref = a * d * np.cos(al) - xt, b * d * np.sin(al) - yt
+    x2, y2 = xt * xt, yt * yt
+    D = a * a * x2 + b * b * y2
+    assert np.all(dstar >= 1.0)
+    np.testing.assert_allclose(xt * b * (a - b) * y2 / D, dx_ref, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(yt * a * (b - a) * x2 / D, dy_ref, rtol=1e-9, atol=1e-12)
+    # fp32: rewritten vs direct
+    f32 = np.float32
+    a32, b32, x32, y32 = a.astype(f32), b.astype(f32), xt.astype(f32), yt.astype(f32)
+    X2, Y2 = x32 * x32, y32 * y32
+    D32 = a32 * a32 * X2 + b32 * b32 * Y2
+    N32 = a32 * X2 + b32 * Y2
+    rw = x32 * ((b32 * (a32 - b32)) * Y2 * (f32(1) / D32))
+    direct = x32 * (a32 * (N32 / D32) - f32(1))
+    big = np.abs(dx_ref) > 1e-3 * np.abs(xt) * (a - b) / a   # away from the axes
+    err_rw = np.abs(rw.astype(np.float64) - dx_ref)[big] / np.abs(dx_ref[big])
+    err_direct = np.abs(direct.astype(np.float64) - dx_ref)[big] / np.abs(dx_ref[big])
+    assert np.median(err_rw) < 3e-7 and np.percentile(err_rw, 99) < 2e-6
+    assert np.median(err_direct) > 100 * np.median(err_rw)
