@@ -33,7 +33,11 @@
  * context's argmin workspace); bmc_solve_host has a workspace of its own and
  * may overlap them, also from another thread (the context's host-side state is
  * locked; host solves on one context run one at a time).  A constant blob
- * uploaded on one stream is waited for (event) by solves on another.
+ * uploaded on one stream is waited for (event) by solves on another until the
+ * upload is known complete.  CUDA graphs: once a context has solved a given
+ * obstacle count (constants uploaded and complete, shared-memory opt-in set),
+ * bmc_solve issues only the kernel launch on the stream and can be captured
+ * (tests/test_gpu_context.py).
  * bmc_last_error() is thread-local.
  *
  * Determinism: an instance's outputs depend on its own inputs, the context and

@@ -58,6 +58,9 @@ struct Blob {
   int blockdiag = 0;
   unsigned long long used = 0;  // LRU tick
   cudaEvent_t ready = nullptr;  // recorded after the upload: solves on other streams wait for it
+  cudaStream_t upload_stream = nullptr;
+  bool uploaded = false;        // the upload is known complete: no wait needed (and none issued,
+                                // so steady-state solves can be captured into a CUDA graph)
 };
 
 void free_blob(Blob& b) {
@@ -286,6 +289,7 @@ static int32_t get_blob(bmc_ctx* c, int n, cudaStream_t stream, Blob** out) {
     free_blob(b);
     return cuda_fail(e, "cudaMemcpyAsync(blob)");
   }
+  b.upload_stream = stream;
   c->blobs[n] = b;
   *out = &c->blobs[n];
   return BMC_OK;
@@ -367,8 +371,16 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
   int32_t rc = get_blob(c, pr->n_obs, s, &blob);
   if (rc != BMC_OK) return rc;
   // the upload may have been issued on another stream (bmc_solve vs bmc_solve_host)
-  cudaError_t ew = cudaStreamWaitEvent(s, blob->ready, 0);
-  if (ew != cudaSuccess) return cuda_fail(ew, "cudaStreamWaitEvent(blob)");
+  if (!blob->uploaded) {
+    if (blob->upload_stream != s) {
+      cudaError_t ew = cudaStreamWaitEvent(s, blob->ready, 0);
+      if (ew != cudaSuccess) return cuda_fail(ew, "cudaStreamWaitEvent(blob)");
+    }
+    if (cudaEventQuery(blob->ready) == cudaSuccess)
+      blob->uploaded = true;
+    else
+      cudaGetLastError();   // cudaErrorNotReady is a status, not an error
+  }
   int ipc = 1, team = 1;
   launch_shape(c, pr->B, pr->team, &ipc, &team);
   while (ipc > 1 && kernel_smem_bytes(c->QP, pr->n_obs, ipc, team) > 227 * 1024) --ipc;

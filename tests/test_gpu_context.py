@@ -87,3 +87,34 @@ def test_host_and_device_solves_from_two_threads():
     for n, g in got_dev + got_host:
         for k in ("coeffs", "lambda_out", "residual", "cost", "best"):
             assert np.array_equal(g[k], ref[n][k]), (n, k)
+
+
+def test_solve_captured_in_a_cuda_graph():
+    """After one warm-up solve (constants uploaded, shared-memory opt-in set), a solve is
+    stream-ordered work only: captured into a CUDA graph and replayed, it writes the same
+    bits as a direct solve, batch argmin included (the last CTA resets the workspace)."""
+    from paper_2109_13030_b200 import solver_for
+    cfg = CONFIGS["C2"].with_(B=64, K=12)
+    pr = make_problem(cfg, 7)
+    s = solver_for(cfg, device=0)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    init, obs, ab = d(pr["init"]), d(pr["obs_xy"]), d(pr["obs_ab"])
+    ref = s.solve(init, obs, ab, pr["bnd"], cfg.K)
+    torch.cuda.synchronize()
+    ref = {k: v.clone() for k, v in ref.items()}
+    out = {k: torch.empty_like(v) for k, v in ref.items()}
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):   # warm-up on the capture stream
+        s.solve(init, obs, ab, pr["bnd"], cfg.K, out=out, stream=side)
+    torch.cuda.synchronize()
+    for v in out.values():
+        v.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        s.solve(init, obs, ab, pr["bnd"], cfg.K, out=out, stream=torch.cuda.current_stream())
+    assert s.last_launches == 1
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        for k in ref:
+            assert torch.equal(out[k], ref[k]), k
