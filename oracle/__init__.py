@@ -10,9 +10,11 @@ the equation map and the readings G1..G18).
 Parity status per function:
   basis, KKT steps, projections, lambda and lambda_psi steps, cost J,
   obstacle-free fixed point, invariants, worked-scene residual decay: pinned by
-  tests/test_oracle_*.py.  Exact iterates on cluttered scenes: parity unpinned
-  by the paper (it prints no worked iterate); pinned only through the
-  invariants above.
+  tests/test_oracle_*.py.  Iterates on cluttered scenes: the paper prints no
+  worked iterate; they are pinned as the composition of the pinned steps in
+  the paper's order (test_iteration_wiring_on_a_cluttered_scene: every
+  iterate recomputed from its predecessor with the pinned steps and an
+  independent BPoly basis) and through the invariants above.
 
 fp32 rounding model (OracleParams.fp32_model / noise_seed, oracle.h): the same
 iteration with every quantity the product path holds in fp32 rounded where it

@@ -223,3 +223,30 @@ def test_g_rows_are_geometric_projections(scene):
             assert np.allclose(g[R + r0:R + r0 + q], obs[j, 1] + dy * scale, atol=1e-9)
     assert np.allclose(g[2 * q + m * n * q:R], np.cos(psi), atol=1e-12)
     assert np.allclose(g[R + 2 * q + m * n * q:], np.sin(psi), atol=1e-12)
+
+
+def test_iteration_wiring_on_a_cluttered_scene(scene):
+    """Every iterate of a cluttered scene (5 obstacles, 3 circles) is the composition of
+    the separately pinned steps in the paper's order (Algorithm of P:371-381): xi1^{k+1}
+    from (lambda^k, g^k) (Eq. 13, pinned by KKT optimality), theta^{k+1} = atan2 of the
+    copies of xi1^{k+1} evaluated with the scipy BPoly basis (Eq. 19), xi2^{k+1} from
+    (lambda_psi^k, theta^{k+1}) (Eq. 18, pinned by KKT optimality), g^{k+1} from the
+    trajectory of (xi1^{k+1}, xi2^{k+1}) (test_g_rows_are_geometric_projections),
+    lambda^{k+1} (test_trace_lambda_consistent_with_step) and lambda_psi^{k+1} =
+    lambda_psi^k - rho_psi P^T (P xi2^{k+1} - theta^{k+1}) with the BPoly basis (Eq. 23b,
+    G4).  A loop that fed a stale iterate to any step fails here."""
+    cfg, pr, o, tr = scene
+    t = np.linspace(0, cfg.T, cfg.q)
+    P = np.stack([eval_bpoly(np.eye(11)[k], cfg.T, t) for k in range(11)], axis=1)   # q x 11
+    bnd = pr["bnd"]
+    for k in range(tr["xi1"].shape[0] - 1):
+        lam, lampsi = tr["lam"][k][:44], tr["lam"][k][44:]
+        xi1 = o.xi1_step(lam, tr["g"][k], bnd)
+        assert np.allclose(xi1, tr["xi1"][k + 1], rtol=0, atol=1e-9 * max(1.0, np.abs(xi1).max())), k
+        cc, ss = P @ xi1[11:22], P @ xi1[33:44]
+        theta = np.arctan2(ss, cc)
+        assert np.allclose(theta, tr["theta"][k + 1], atol=1e-10), k
+        xi2 = o.xi2_step(lampsi, theta, bnd)
+        assert np.allclose(xi2, tr["xi2"][k + 1], atol=1e-9), k
+        lampsi_next = lampsi - cfg.rho_psi * (P.T @ (P @ xi2 - theta))
+        assert np.allclose(lampsi_next, tr["lam"][k + 1][44:], atol=1e-9 * max(1.0, np.abs(lampsi_next).max())), k
