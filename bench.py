@@ -50,14 +50,53 @@ def fp32_peak(sm_mhz: float, sms: int = 148) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled every
+    0.5 ms from a thread (a C3 region is ~10 ms), and nvidia-smi (100 ms period) as
+    the fallback when NVML is unavailable or saw fewer than 3 samples."""
+
+    NVML_PERIOD_S = 5e-4
 
     def __init__(self, gpus):
         self.gpus = gpus
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        self.nv = []            # (sm_mhz, reasons bitmask) from NVML
+        self.nv_max = None
+        self._stop = None
+        self._thread = None
+
+    def _nvml_start(self):
+        import threading
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        h = None
+        try:   # the CUDA device's own NVML handle (CUDA_VISIBLE_DEVICES may renumber)
+            uuid = str(torch.cuda.get_device_properties(self.gpus[0]).uuid)
+            h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpus[0])
+        self.nv_max = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.nv.append((float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), int(reasons_fn(h))))
+                except Exception:
+                    return
+                time.sleep(self.NVML_PERIOD_S)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
 
     def __enter__(self):
+        try:
+            self._nvml_start()
+        except Exception:
+            self._thread = None
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
@@ -72,6 +111,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -81,6 +123,15 @@ class ClockSampler:
             self.f.close()
 
     def summary(self):
+        if len(self.nv) >= 3:
+            import pynvml
+            bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+            reasons = sorted(nm for nm, b in bits.items() if any(r & b for _, r in self.nv))
+            return {"sm_mhz": statistics.median(v for v, _ in self.nv), "sm_max_mhz": self.nv_max,
+                    "reasons": reasons, "samples": len(self.nv), "sampler": "nvml, 0.5 ms"}
         if self.proc is None or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], [], set()
