@@ -516,12 +516,16 @@ static int32_t solve_impl(bmc_ctx* c, const bmc_problem* pr, const bmc_result* r
       }
       tt.push_back(mx / (pr->iters + 1));
     }
-    if (const char* fn = std::getenv("BMC_PROF_DUMP")) {   // per team (= instance): loop cycles/iter, tested
-      if (FILE* f = std::fopen(fn, "w")) {
+    if (const char* fn = std::getenv("BMC_PROF_DUMP")) {   // per team (= instance): loop cycles/iter, tested,
+      if (FILE* f = std::fopen(fn, "w")) {                 // then per rank: D1 cycles/iter and tested
         for (size_t i = 0; i < tt.size(); ++i) {
           long long tested = 0;
           for (int wv = 0; wv < team; ++wv) tested += hp[(i * team + wv) * 16 + 9];
-          std::fprintf(f, "%zu %.1f %lld\n", i, tt[i], tested);
+          std::fprintf(f, "%zu %.1f %lld", i, tt[i], tested);
+          for (int wv = 0; wv < team; ++wv)
+            std::fprintf(f, " %.1f %lld", (double)hp[(i * team + wv) * 16 + 10] / (pr->iters + 1),
+                         hp[(i * team + wv) * 16 + 9]);
+          std::fprintf(f, "\n");
         }
         std::fclose(f);
       }
